@@ -1,0 +1,644 @@
+#!/usr/bin/env python
+"""Benchmark of the fp64 tensor-Chebyshev hot path (BASELINE.json metric: Chebyshev evals/s and
+game time-steps/s, fp64, 1/2/4/8 B200 vs CPU).
+
+Default workload = BASELINE configs[1] ("config 2"): J=3, n=33 (35,937 coefficients), node values
+exp(-sum b_j (x_j - c_j)^2), M = 2^20 scattered points per GPU.  One step = build the coefficient
+tensor from the node values (K1) + evaluate it at the M points (K2).  `value` = evals/s of the
+whole job (weak scaling: every rank evaluates its own 2^20 points), measured with CUDA events
+per step, max over ranks.  `e2e` = the same through the public API with host (pinned) inputs and
+outputs, H2D / D2H inside the timed region.  --config selects the other BASELINE configs
+(3 / 5b report steps/s of the time loop; 5a reports structured evals/s).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+Under torchrun (N > 1) each rank drives one GPU; the loop configs shard nodes and all-gather
+node values over NCCL once per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+# CPU baseline: the reference's own parallel scheme (thread pool, 1 BLAS thread per worker,
+# S/solver.py:423-437).  Must be set before numpy is imported.
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+os.environ.setdefault("OMP_NUM_THREADS", "1")
+
+import numpy as np  # noqa: E402
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "Chebyshev evals/sec & game time-steps/sec (fp64) at 1/2/4/8 B200 vs CPU"
+FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+
+
+def algorithmic_eval_flops(J: int, n: int) -> int:
+    """2 * sum_{m=1..J} n^m flops per point."""
+    return 2 * sum(n ** m for m in range(1, J + 1))
+
+
+def measured_peaks():
+    peaks = {"hbm_gbs": None, "fp64_tflops": None, "fp64_source": None, "hbm_source": None}
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            mp = json.load(f)
+        peaks["hbm_gbs"] = mp.get("hbm_gbs")
+        peaks["hbm_source"] = "MEASURED_PEAKS.json hbm_gbs (measured)"
+    if peaks["hbm_gbs"] is None:
+        peaks["hbm_gbs"] = 6650.0
+        peaks["hbm_source"] = "B200_PROFILING.md fallback 6.65 TB/s"
+    if os.path.exists(FP64_PEAK_FILE):
+        with open(FP64_PEAK_FILE) as f:
+            fp = json.load(f)
+        peaks["fp64_tflops"] = fp["fp64_peak_tflops"]
+        peaks["fp64_source"] = fp["source"]
+    else:
+        peaks["fp64_tflops"] = 37.0
+        peaks["fp64_source"] = "tools/microbench/fp64_peak.cu DMMA sustained (measured r01)"
+    return peaks
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, ValueError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": max(smax) if smax else None,
+            "reasons": sorted(reasons),
+            "samples": len(sm),
+        }
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def max_over_ranks(x: float, world: int, torch):
+    if world == 1:
+        return x
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU baseline (oracle port of the reference algorithm) — the one place bench.py runs oracle/
+# ------------------------------------------------------------------------------------------------
+
+def cpu_baseline(cfg: str, budget_s: float = 12.0):
+    from oracle import cheb_oracle as orc
+    from paper_2307_04688_b200 import workloads
+
+    cores = os.cpu_count() or 1
+    if cfg in ("1", "2", "4"):
+        w = workloads.make(cfg, M=16)
+        full_M = {"1": 65_536, "2": 1 << 20, "4": 1 << 24}[cfg]
+        rng = np.random.default_rng(7)
+        # calibrate a sample that takes ~budget_s
+        sample = 256
+        pts = 2.0 * rng.random((sample, w.J)) - 1.0
+        t0 = time.perf_counter()
+        C = orc.tensor_coeffs(w.values)
+        tb = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        orc.eval_points_parallel(C, pts, workers=cores, block=64)
+        te = time.perf_counter() - t0
+        per_pt = te / sample
+        sample = int(min(full_M, max(256, (budget_s - tb) / max(per_pt, 1e-9))))
+        pts = 2.0 * rng.random((sample, w.J)) - 1.0
+        t0 = time.perf_counter()
+        C = orc.tensor_coeffs(w.values)
+        tb = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        orc.eval_points_parallel(C, pts, workers=cores, block=max(64, sample // (4 * cores)))
+        te = time.perf_counter() - t0
+        # full step = one build + full_M evals, extrapolated linearly from the sample
+        step_s = tb + te * (full_M / sample)
+        return {
+            "value": full_M / step_s,
+            "unit": "evals/s",
+            "cores": cores,
+            "kind": "port",
+            "sample": f"oracle tensor_coeffs + eval of {sample} seeded points on {cores} threads "
+                      f"(ThreadPool, OPENBLAS_NUM_THREADS=1), extrapolated to M={full_M}",
+            "step_seconds": step_s,
+        }
+    if cfg in ("3", "5b"):
+        w = workloads.make(cfg)
+        T, S = orc.advect_points(w.values.shape, w.A, w.dt)
+        N = T.shape[0]
+        t0 = time.perf_counter()
+        C = orc.tensor_coeffs(w.values)
+        tb = time.perf_counter() - t0
+        sample = 512
+        t0 = time.perf_counter()
+        orc.eval_points_parallel(C, T[:sample], workers=cores, block=32)
+        per_pt = (time.perf_counter() - t0) / sample
+        sample = int(min(N, max(512, (budget_s - tb) / max(per_pt, 1e-9))))
+        t0 = time.perf_counter()
+        orc.eval_points_parallel(C, T[:sample], workers=cores, block=max(32, sample // (4 * cores)))
+        te = time.perf_counter() - t0
+        step_s = tb + te * (N / sample)
+        return {
+            "value": 1.0 / step_s,
+            "unit": "steps/s",
+            "cores": cores,
+            "kind": "port",
+            "sample": f"oracle build + {sample} of {N} advected nodes on {cores} threads, extrapolated to one step",
+            "step_seconds": step_s,
+        }
+    # 5a structured
+    w = workloads.make("5a")
+    t0 = time.perf_counter()
+    C = orc.tensor_coeffs(w.values)
+    k = 25
+    # sample: grid restricted to the first 5 targets of the first axis (1/5 of the work), x5
+    targets = [w.targets[0][:5]] + list(w.targets[1:])
+    orc.eval_grid(C, targets)
+    el = time.perf_counter() - t0
+    step_s = el * (k / 5)
+    return {
+        "value": k ** 6 / step_s,
+        "unit": "evals/s",
+        "cores": 1,
+        "kind": "port",
+        "sample": "oracle build + eval_grid on a 5x25^5 slice of the 25^6 grid (numpy matmul, 1 BLAS thread), x5",
+        "step_seconds": step_s,
+    }
+
+
+def run_reference(args):
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    cfg = args.config
+    steps = []
+    for _ in range(args.warmup):
+        cpu_baseline(cfg, budget_s=2.0)
+    for _ in range(args.steps):
+        steps.append(cpu_baseline(cfg, budget_s=args.cpu_budget))
+    vals = [s["value"] for s in steps]
+    v = statistics.median(vals)
+    base = steps[0]
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": v,
+        "unit": base["unit"],
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1000.0 * statistics.median(s["step_seconds"] for s in steps),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE.json shapes)",
+        "config": workload_config(cfg, 1),
+        "cpu_baseline": {"value": v, "unit": base["unit"], "cores": base["cores"], "kind": base["kind"],
+                         "sample": base["sample"]},
+        "e2e": {"value": v, "unit": base["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(cfg: str, world: int):
+    from paper_2307_04688_b200 import workloads  # noqa: F401
+
+    desc = {
+        "1": {"workload": "config1: J=2 n=17 build + eval at M=65,536 points/GPU", "J": 2, "n": 17, "M": 65_536},
+        "2": {"workload": "config2: J=3 n=33 build + eval at M=2^20 points/GPU", "J": 3, "n": 33, "M": 1 << 20},
+        "3": {"workload": "config3: J=4 n=17 advected-node time step (build + eval of 83,521 nodes)", "J": 4,
+              "n": 17, "M": 17 ** 4},
+        "4": {"workload": "config4: J=5 n=17 build + eval at M=2^24 points/GPU", "J": 5, "n": 17, "M": 1 << 24},
+        "5a": {"workload": "config5a: J=6 n=13 build + structured eval on a 25^6 grid", "J": 6, "n": 13,
+               "M": 25 ** 6},
+        "5b": {"workload": "config5b: J=6 n=13 advected-node time step (4,826,809 nodes)", "J": 6, "n": 13,
+               "M": 13 ** 6},
+    }[cfg]
+    d = dict(desc)
+    d["parallelism"] = f"dp{world}" if cfg in ("1", "2", "4", "5a") else f"node-shard{world}+allgather"
+    d["l2_flush"] = "256 MiB write between timed steps"
+    return d
+
+
+# ------------------------------------------------------------------------------------------------
+# GPU arm
+# ------------------------------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2307_04688_b200 as cn
+    from paper_2307_04688_b200 import _lib, workloads
+    from paper_2307_04688_b200.chebnd import _eval_points_device, tensor_coeffs_device
+
+    lib = _lib.load()
+    cfg = args.config
+    peaks = measured_peaks()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+    launches0 = None
+
+    if cfg in ("1", "2", "4"):
+        w = workloads.make(cfg)
+        J, n = w.J, w.n
+        shape = (n,) * J
+        M = w.M
+        # every rank evaluates its own block of M points (weak scaling); rank r uses a shifted
+        # copy of the seeded points so ranks do distinct work
+        pts_host = np.ascontiguousarray(np.roll(w.points, rank * 977, axis=0))
+        vals_dev = _lib.to_device(w.values)
+        pts_dev = _lib.to_device(pts_host)
+        L = _lib.eval_layout(shape)
+        coef = _lib.empty((L["elems"],))
+        out = _lib.empty((M,))
+        st = _lib.new_status()
+
+        def step():
+            tensor_coeffs_device(vals_dev, shape, out=coef, status=st)
+            e_mid.record(stream)
+            _eval_points_device(shape, coef, pts_dev, check=False, out=out)
+
+        e0 = torch.cuda.Event(enable_timing=True)
+        e_mid = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        barrier(world)
+        torch.cuda.synchronize()
+        clocks = ClockSampler(local)
+        clocks.start()
+        launches0 = int(lib.cb_kernel_launches())
+        build_ms, eval_ms, step_ms = [], [], []
+        for _ in range(args.steps):
+            flush.zero_()
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            e1.synchronize()
+            build_ms.append(e0.elapsed_time(e_mid))
+            eval_ms.append(e_mid.elapsed_time(e1))
+            step_ms.append(e0.elapsed_time(e1))
+        torch.cuda.synchronize()
+        launches = int(lib.cb_kernel_launches()) - launches0
+        barrier(world)
+        torch.cuda.synchronize()
+        clk = clocks.stop()
+        t_total = max_over_ranks(sum(step_ms) / 1000.0, world, torch)
+        value = world * M * args.steps / t_total
+        # parity spot-check of this run's output (rank 0, small subset, oracle as checker)
+        flops_pt = algorithmic_eval_flops(J, n)
+        eval_s = statistics.mean(eval_ms) / 1000.0
+        build_s = statistics.mean(build_ms) / 1000.0
+        achieved_tf = flops_pt * M / eval_s / 1e12
+        roofline = {
+            "bound": "fp64", "kernel": "eval_dmma_kernel (K2, DMMA.8x8x4)",
+            "achieved": achieved_tf, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+            "frac": achieved_tf / peaks["fp64_tflops"], "peak_source": peaks["fp64_source"],
+            "algorithmic": f"{flops_pt} flop/point x {M} points per launch",
+            "traffic": ncu_traffic("eval_dmma_kernel", cfg),
+        }
+        build_bytes = 16 * n ** J
+        roofline_build = {
+            "bound": "hbm", "kernel": "build_pass_kernel (K1)", "achieved": build_bytes / build_s / 1e9,
+            "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": build_bytes / build_s / 1e9 / peaks["hbm_gbs"],
+            "algorithmic": f"16*n^J = {build_bytes} bytes per build", "ms": build_s * 1000.0,
+        }
+        # ---------------- e2e through the public API with pinned host buffers ----------------
+        vals_pin = torch.from_numpy(np.ascontiguousarray(w.values)).pin_memory()
+        pts_pin = torch.from_numpy(pts_host).pin_memory()
+        bases = [cn.make_basis(n - 1, 0.0, 1.0)] * J
+        res = None
+        for _ in range(max(1, args.warmup)):
+            res = cn.eval_points(cn.tensor_coeffs(vals_pin, bases), pts_pin)
+        barrier(world)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            res = cn.eval_points(cn.tensor_coeffs(vals_pin, bases), pts_pin)  # returns pinned host tensor
+        torch.cuda.synchronize()
+        e2e_s = max_over_ranks(time.perf_counter() - t0, world, torch)
+        e2e = {"value": world * M * args.steps / e2e_s, "unit": "evals/s",
+               "h2d_bytes_per_step": int(vals_pin.numel() * 8 + pts_pin.numel() * 8),
+               "d2h_bytes_per_step": int(res.numel() * 8 + 16)}
+        # parity of the e2e result against the device-timed output and the oracle on a subset
+        parity = None
+        if rank == 0:
+            from oracle import cheb_oracle as orc
+
+            C = orc.tensor_coeffs(w.values)
+            sub = slice(0, 2048)
+            ref = orc.eval_points(C, pts_host[sub])
+            got = res.numpy()[sub]
+            parity = {"max_abs": float(np.abs(got - ref).max()),
+                      "allclose_1e-12_1e-11": bool(np.allclose(got, ref, rtol=1e-12, atol=1e-11)),
+                      "device_vs_e2e_bitwise": bool(np.array_equal(_lib.to_host(out)[sub], got))}
+        unit = "evals/s"
+        extra = {"roofline_build": roofline_build, "parity_check": parity,
+                 "eval_ms": statistics.mean(eval_ms), "build_ms": statistics.mean(build_ms)}
+        ms_per_step = 1000.0 * t_total / args.steps
+    elif cfg in ("3", "5b"):
+        from paper_2307_04688_b200.dist import ShardedAdvectLoop
+        from paper_2307_04688_b200.loop import CudaStepBackend
+
+        w = workloads.make(cfg)
+        J, n = w.J, w.n
+        shape = (n,) * J
+        N = n ** J
+        bases = [cn.make_basis(n - 1, 0.0, 1.0)] * J
+        steps_per_iter = 1
+        if world == 1:
+            vals = _lib.to_device(w.values).clone()
+            tmp = _lib.empty(shape)
+            L = _lib.eval_layout(shape)
+            coef = _lib.empty((L["elems"],))
+
+            def run_steps(k):
+                lib.cb_advect_loop(J, _lib.i64_array(shape), _lib.ptr(vals), _lib.ptr(tmp), _lib.ptr(coef), k,
+                                   _lib.dbl_array(w.A), w.dt, _lib.dbl_array([0.0] * J), _lib.dbl_array([1.0] * J),
+                                   None, 1, _lib.stream_handle())
+        else:
+            backend = CudaStepBackend(bases, w.A, w.dt)
+            loop = ShardedAdvectLoop(shape, backend)
+
+            def run_steps(k):
+                loop.run(w.values, k)
+        # the BASELINE loop length: 100 steps (cfg 3) / 20 steps (cfg 5b) per timed step
+        inner = w.steps
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        for _ in range(args.warmup):
+            run_steps(inner)
+        torch.cuda.synchronize()
+        barrier(world)
+        torch.cuda.synchronize()
+        clocks = ClockSampler(local)
+        clocks.start()
+        launches0 = int(lib.cb_kernel_launches())
+        times = []
+        for _ in range(args.steps):
+            flush.zero_()
+            e0.record(stream)
+            run_steps(inner)
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+        torch.cuda.synchronize()
+        launches = int(lib.cb_kernel_launches()) - launches0
+        barrier(world)
+        clk = clocks.stop()
+        t_total = max_over_ranks(sum(times) / 1000.0, world, torch)
+        total_steps = inner * args.steps
+        value = total_steps / t_total
+        unit = "steps/s"
+        # per-kernel timing of one step (isolated events) for the roofline
+        M = N
+        flops_pt = algorithmic_eval_flops(J, n)
+        from paper_2307_04688_b200.chebnd import tensor_coeffs_device as tcd
+
+        L = _lib.eval_layout(shape)
+        cbuf = _lib.empty((L["elems"],))
+        vbuf = _lib.to_device(w.values)
+        obuf = _lib.empty((N,))
+        ea, eb, ec = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        bl, ev = [], []
+        for _ in range(3):
+            ea.record(stream)
+            tcd(vbuf, shape, out=cbuf)
+            eb.record(stream)
+            lib.cb_eval_advected(J, _lib.i64_array(shape), _lib.ptr(cbuf), 0, N, _lib.dbl_array(w.A), w.dt,
+                                 _lib.dbl_array([0.0] * J), _lib.dbl_array([1.0] * J), 1, _lib.ptr(obuf),
+                                 _lib.stream_handle())
+            ec.record(stream)
+            ec.synchronize()
+            bl.append(ea.elapsed_time(eb))
+            ev.append(eb.elapsed_time(ec))
+        eval_s = min(ev) / 1000.0
+        build_s = min(bl) / 1000.0
+        achieved_tf = flops_pt * M / eval_s / 1e12
+        roofline = {
+            "bound": "fp64", "kernel": "eval_dmma_kernel (K2, advected nodes)", "achieved": achieved_tf,
+            "peak": peaks["fp64_tflops"], "unit": "TFLOP/s", "frac": achieved_tf / peaks["fp64_tflops"],
+            "peak_source": peaks["fp64_source"], "algorithmic": f"{flops_pt} flop/point x {M} nodes per launch",
+            "traffic": ncu_traffic("eval_dmma_kernel", cfg),
+        }
+        build_bytes = 16 * N
+        extra = {"roofline_build": {"bound": "hbm", "kernel": "build_pass_kernel (K1)",
+                                    "achieved": build_bytes / build_s / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                                    "frac": build_bytes / build_s / 1e9 / peaks["hbm_gbs"], "ms": build_s * 1e3},
+                 "loop_steps_per_timed_step": inner}
+        # e2e: public API advect_loop from host values, result back to host
+        vals_pin = torch.from_numpy(np.ascontiguousarray(w.values)).pin_memory()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            res = cn.advect_loop(vals_pin, bases, w.A, w.dt, inner)
+            if torch.is_tensor(res):
+                res = res.cpu()
+        torch.cuda.synchronize()
+        e2e_s = max_over_ranks(time.perf_counter() - t0, world, torch)
+        e2e = {"value": total_steps / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": int(N * 8 / inner),
+               "d2h_bytes_per_step": int(N * 8 / inner)}
+        ms_per_step = 1000.0 * t_total / total_steps
+    else:  # 5a structured
+        w = workloads.make("5a")
+        J, n = w.J, w.n
+        shape = (n,) * J
+        bases = [cn.make_basis(n - 1, 0.0, 1.0)] * J
+        k = w.params["k"]
+        # shard the first target axis across ranks (outputs stay sharded)
+        from paper_2307_04688_b200.dist import shard_range
+
+        a, b, _ = shard_range(k, rank, world)
+        targets = [w.targets[0][a:b]] + list(w.targets[1:])
+        vals_dev = _lib.to_device(w.values)
+        tdev = [_lib.to_device(t) for t in targets]
+
+        def step():
+            t = cn.tensor_coeffs(vals_dev, bases)
+            return cn.eval_grid(t, tdev)
+
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        barrier(world)
+        clocks = ClockSampler(local)
+        clocks.start()
+        launches0 = int(lib.cb_kernel_launches())
+        times = []
+        for _ in range(args.steps):
+            flush.zero_()
+            e0.record(stream)
+            out_t = step()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+            del out_t
+        launches = int(lib.cb_kernel_launches()) - launches0
+        clk = clocks.stop()
+        t_total = max_over_ranks(sum(times) / 1000.0, world, torch)
+        M = k ** J
+        value = M * args.steps / t_total
+        unit = "evals/s"
+        bytes_alg = 8 * (n ** J + (b - a) * k ** (J - 1))
+        achieved = bytes_alg / (t_total / args.steps) / 1e9
+        roofline = {"bound": "hbm", "kernel": "eval_grid (K3 mode products)", "achieved": achieved,
+                    "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                    "algorithmic": "8*(n^J + k^J) bytes per step", "traffic": ncu_traffic("rotate_fixed", cfg)}
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            res = cn.eval_grid(cn.tensor_coeffs(w.values, bases), targets)
+        e2e_s = max_over_ranks(time.perf_counter() - t0, world, torch)
+        e2e = {"value": M * args.steps / e2e_s, "unit": "evals/s", "h2d_bytes_per_step": int(8 * n ** J),
+               "d2h_bytes_per_step": int(res.size * 8)}
+        extra = {}
+        ms_per_step = 1000.0 * t_total / args.steps
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            cpu = cpu_baseline(cfg, budget_s=args.cpu_budget)
+            cpu = {k2: v2 for k2, v2 in cpu.items() if k2 != "step_seconds"}
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": unit,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": "weak" if cfg in ("1", "2", "4") else "strong",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (seeded numpy, BASELINE.json shapes; no dataset)",
+            "config": workload_config(cfg, world),
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+        }
+        line.update(extra)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def ncu_traffic(kernel: str, cfg: str):
+    """dram read+write bytes per launch of `kernel` from the committed ncu --set full summary."""
+    if not os.path.exists(NCU_SUMMARY):
+        return None
+    try:
+        with open(NCU_SUMMARY) as f:
+            s = json.load(f)
+        return s.get(cfg, {}).get(kernel, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="2", choices=["1", "2", "3", "4", "5a", "5b"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU work per baseline sample")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,145 @@
+/*
+ * chebnash_b200 — C ABI of the B200-native fp64 tensor-Chebyshev engine.
+ *
+ * Drop-in boundary for the hot path of the reference package `chebnash` (arXiv 2307.04688):
+ * J-dimensional tensor-product Chebyshev interpolation inside the time-stepping solver.  The
+ * reference has no FFI layer — its boundary is the Python API re-exported by
+ * pkg/src/chebnash/__init__.py:11-57 — so every entry point below names the reference function
+ * it replaces (file:line, paths relative to pkg/src/chebnash/).  The Python shim
+ * paper_2307_04688_b200/ binds these with ctypes and keeps the reference signatures
+ * (see INTEGRATION.md).
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  `d_*` pointers are device (CUDA global) memory owned by the
+ *     caller; the library never allocates or frees caller memory.  `stream` is a cudaStream_t
+ *     passed as void* (NULL = legacy default stream).  All calls are asynchronous on `stream`.
+ *   - Return value: CB_OK (0) or a CB_E* code; cb_last_error() gives a thread-local message.
+ *   - `d_status` (optional, may be NULL) points to a 16-byte device block
+ *       { uint32 nonfinite; uint32 domain; uint64 worst_abs_bits; }
+ *     that kernels update: nonfinite != 0 -> "must be finite" ValueError; domain != 0 ->
+ *     "evaluation point outside [-1, 1] beyond tolerance: |x| = <worst>" ValueError
+ *     (cheb1d.py:127-135, chebnd.py:179-185).  The caller zeroes it before the call.
+ *   - Dense tensors are C-order (n_1, ..., n_J) fp64 (chebnd.py:33-54).  Coefficients consumed by
+ *     the evaluators are in the "eval layout" described by cb_eval_layout().
+ *   - Re-entrant: no global mutable state apart from per-device kernel attributes.
+ */
+#ifndef CHEBNASH_B200_H
+#define CHEBNASH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CB_ABI_VERSION 1
+
+enum {
+  CB_OK = 0,
+  CB_EINVAL = 1,  /* bad shape / argument (reference raises ValueError) */
+  CB_ECUDA = 4    /* CUDA runtime error */
+};
+
+int cb_abi_version(void);
+const char* cb_last_error(void);
+
+/* Number of kernels this library has launched in the process (graph replays not included). */
+int64_t cb_kernel_launches(void);
+
+/* Device inventory: number of visible CUDA devices (0 without a GPU), SM count and compute
+ * capability of the current device.  Never fails on a CPU-only host. */
+int cb_runtime_info(int* device_count, int* sm_count, int* cc_major, int* cc_minor);
+
+/* Eval layout of a J-mode tensor with sizes n[0..J-1]:
+ *   out[0]=q (trailing modes merged into columns), out[1]=R (rows), out[2]=R8 (rows padded to 8),
+ *   out[3]=K (columns), out[4]=Kp (columns padded to 4), out[5]=R8*Kp (elements to allocate).
+ * Host-only. */
+int cb_eval_layout(int J, const int64_t* n, int64_t* out6);
+
+/* Dense C-order (n_1..n_J) <-> eval layout (zero padding written by pack).  Used when a
+ * CoefTensor is constructed from user coefficients (chebnd.py:33-54) and when its
+ * `.coefficients` are read back. */
+int cb_pack_eval(int J, const int64_t* n, const double* d_dense, double* d_eval, void* stream);
+int cb_unpack_eval(int J, const int64_t* n, const double* d_eval, double* d_dense, void* stream);
+
+/* K1 — tensor_coeffs (chebnd.py:162-190; cheb_transform cheb1d.py:138-170 per mode).
+ * d_samples: dense (n_1..n_J) node values, entry (k_1..k_J) at the descending nodes
+ * (make_basis cheb1d.py:73-104).  d_coef: eval layout, cb_eval_layout()[5] doubles.
+ * Non-finite samples set d_status->nonfinite. */
+int cb_tensor_coeffs(int J, const int64_t* n, const double* d_samples, double* d_coef, void* d_status, void* stream);
+
+/* K1 generic — apply the node->coefficient transform along the consecutive axes [a0, a1) of a
+ * dense C-order array of `ndim` dims.  Covers stack_coeffs (chebnd.py:193-206: axes 0..J-1 of
+ * (n_1..n_J, N_P)), cheb_transform(values, axis) (cheb1d.py:138-170: one axis) and
+ * coeffs_from_samples (cheb1d.py:173-195).  d_out may equal d_in. */
+int cb_transform_axes(int ndim, const int64_t* shape, int a0, int a1, const double* d_in, double* d_out,
+                      void* d_status, int check_finite, void* stream);
+
+/* K2 — batched scattered evaluation: the solver's value evaluator solver.py:388-397 with the
+ * semantics of eval_full chebnd.py:315-327 (clamp_reference cheb1d.py:127-135).
+ * d_points: (M, J) row-major reference coordinates in [-1, 1]; d_out: (M,).
+ * flags bit 0: force the DFMA fallback kernel (testing). */
+int cb_eval_points(int J, const int64_t* n, const double* d_coef, int64_t M, const double* d_points, double* d_out,
+                   void* d_status, int flags, void* stream);
+
+/* K4 building block — evaluate at advected grid nodes (solver.py:383-397 with a fixed linear
+ * drift): for flat C-order node indices i in [node_begin, node_begin+count):
+ *   x = grid node i on the box [lo, hi]^J (make_basis nodes), y = clip(x + dt*A x, lo, hi),
+ *   d_out[i - node_begin] = V(y) - (source ? dt*|x|^2 : 0),  V given by d_coef (eval layout).
+ * A: host J x J row-major.  lo, hi: host arrays of J. */
+int cb_eval_advected(int J, const int64_t* n, const double* d_coef, int64_t node_begin, int64_t count,
+                     const double* A, double dt, const double* lo, const double* hi, int source, double* d_out,
+                     void* stream);
+
+/* K4 — device-resident time loop on one GPU (solver.py:541-550 skeleton, BASELINE configs 3/5b):
+ *   repeat `steps` times:  C = tensor_coeffs(V);  V <- eval_advected(C) (source on).
+ * d_values: dense (n_1..n_J) V_0 in, V_steps out.  d_tmp: same size scratch.  d_coef: eval-layout
+ * scratch.  use_graph != 0 captures the step pair in a CUDA graph (no per-step host work). */
+int cb_advect_loop(int J, const int64_t* n, double* d_values, double* d_tmp, double* d_coef, int steps,
+                   const double* A, double dt, const double* lo, const double* hi, void* d_status, int use_graph,
+                   void* stream);
+
+/* Single-axis contraction with an evaluation matrix E (k x n, row-major):
+ *   out[a*oA + j*oJ + r*oR + q] = sum_l E[j*n + l] * in[((a*n + l)*R + r)*Q + q]
+ * eval_axis (chebnd.py:209-240) = (A=1, Q=1 | Q=N_P, oR=k*Q, oJ=Q ...), _bind_rows (:152-154),
+ * _bind_shared (:147-149). */
+int cb_contract_axis(int64_t A, int n, int64_t R, int64_t Q, int k, const double* d_E, const double* d_in,
+                     double* d_out, int64_t oA, int64_t oJ, int64_t oR, void* stream);
+
+/* Diagonal contraction: out[m*oM + r*oR] = sum_l w_{m,l} * in[m*sM + l*sL + r*sR] with
+ * w_{m,l} = T_l(x_m) (x clamped like clamp_reference when clamp != 0) or, when d_W is non-NULL,
+ * w_{m,l} = d_W[m*n + l].  eval_diagonal_batch (chebnd.py:275-312), _bind_diagonal (:157-159),
+ * clenshaw with batch axes (cheb1d.py:198-214). */
+int cb_contract_diagonal(int64_t M, int n, int64_t R, const double* d_x, const double* d_W, int clamp,
+                         const double* d_in, int64_t sM, int64_t sL, int64_t sR, double* d_out, int64_t oM, int64_t oR,
+                         void* d_status, void* stream);
+
+/* derivative_array (cheb1d.py:230-249): rows of L coefficients -> rows of L-1 derivative
+ * coefficients (reference variable). */
+int cb_derivative(int64_t rows, int L, const double* d_in, double* d_out, void* stream);
+
+/* basis_matrix (chebnd.py:114-132; clamp != 0) and _row_basis (:135-144; clamp == 0):
+ * d_out (k, size) row-major, B[j, l] = T_l(x_j). */
+int cb_basis_matrix(int64_t k, const double* d_x, int size, double* d_out, void* d_status, int clamp, void* stream);
+
+/* make_gather_index (chebnd.py:243-272): d_flat[i] = (i % rest) + rest*(count+1)*(i / rest). */
+int cb_gather_index(int64_t rest, int64_t count, int64_t* d_flat, void* stream);
+
+/* GatherIndex.take (chebnd.py:97-111): Fortran-order gather between C-contiguous arrays:
+ * out_F[i] = in_F[flat[i]] for i < nsel. */
+int cb_gather_take(int ndim_in, const int64_t* shape_in, const double* d_in, int64_t nsel, const int64_t* d_flat,
+                   int ndim_out, const int64_t* shape_out, double* d_out, void* stream);
+
+/* K3 — structured evaluation on a tensor-product target grid: J successive eval_axis mode
+ * products (chebnd.py:209-233; paper pagemtimes P:385-417).  d_E[j]: device (k_j x n_j)
+ * row-major evaluation matrices T_l(t_{j,i}).  d_out: dense (k_1..k_J).  d_work: scratch of
+ * cb_eval_grid_workspace() doubles. */
+int64_t cb_eval_grid_workspace(int J, const int64_t* n, const int64_t* k);
+int cb_eval_grid(int J, const int64_t* n, const double* d_coef, const int64_t* k, const double* const* d_E,
+                 double* d_out, double* d_work, int64_t work_elems, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CHEBNASH_B200_H */

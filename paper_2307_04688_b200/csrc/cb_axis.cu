@@ -1,0 +1,357 @@
+// K3 (structured evaluation) and the single-axis contractions behind the stack / axis API.
+//
+//   contract_axis     : out[a, j, r, q] (any strides) = sum_l E[j, l] in[a, l, r, q]
+//                       - eval_axis on a CoefTensor (S/chebnd.py:209-233, _bind_rows :152-154)
+//                         = A=1, Q=1, out (rest, k) "rotated";
+//                       - eval_axis on a TensorStack (:234-240, _bind_shared :147-149) = Q = N_P;
+//                       - _bind_shared / _bind_rows layouts directly.
+//   contract_diagonal : out[m, r] = sum_l T_l(x_m) in[m, l, r]   (eval_diagonal_batch :275-312,
+//                       _bind_diagonal :157-159) with arbitrary strides.
+//   eval_grid         : J successive rotating mode products with k_j x n_j evaluation matrices
+//                       (the paper's pagemtimes evaluation P:385-417; BASELINE config 5a).
+//   basis_matrix, gather_index, gather_take_f : S/chebnd.py:114-132, 243-272, 97-111.
+#include "cb_common.cuh"
+#include "cb_kernels.h"
+
+namespace cb {
+
+namespace {
+
+constexpr int kAxThreads = 256;
+
+struct AxisParams {
+  const double* E;
+  const double* in;
+  double* out;
+  long long A, R, Q;
+  int n, k;
+  long long oA, oJ, oR;
+  long long total;  // A*k*R*Q
+};
+
+// generic: one thread per output element, q fastest then r, j, a
+__global__ void __launch_bounds__(kAxThreads) contract_axis_generic(AxisParams p) {
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < p.total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    long long q = e % p.Q;
+    long long t = e / p.Q;
+    long long r = t % p.R;
+    t /= p.R;
+    int j = static_cast<int>(t % p.k);
+    long long a = t / p.k;
+    const double* src = p.in + (a * p.n * p.R + r) * p.Q + q;
+    const double* er = p.E + static_cast<long long>(j) * p.n;
+    double acc = 0.0;
+    for (int l = 0; l < p.n; ++l) acc = fma(__ldg(er + l), src[static_cast<long long>(l) * p.R * p.Q], acc);
+    p.out[a * p.oA + j * p.oJ + r * p.oR + q] = acc;
+  }
+}
+
+// Fast rotating product (A = 1, Q = 1): in (n, R) -> out (R, k), out[r, j] = sum_l E[j, l] in[l, r].
+// A CTA owns kRT consecutive r; each thread keeps 2 input columns in registers (compile-time n)
+// and produces their k outputs; the (kRT x k) output tile is staged in smem and stored
+// contiguously (the tile is a contiguous block of the output).
+constexpr int kRT = 256;   // rows per CTA (2 per thread, 128 threads)
+constexpr int kRotThreads = 128;
+
+template <int NT>
+__global__ void __launch_bounds__(kRotThreads) rotate_fixed(const double* __restrict__ E, const double* __restrict__ in,
+                                                            double* __restrict__ out, long long R, int k) {
+  extern __shared__ __align__(16) double sm[];
+  double* Es = sm;                         // [k][NT]
+  double* Os = sm + ((k * NT + 1) & ~1);   // [kRT][k]
+  for (int e = threadIdx.x; e < k * NT; e += blockDim.x) Es[e] = E[e];
+  for (long long r0 = static_cast<long long>(blockIdx.x) * kRT; r0 < R; r0 += static_cast<long long>(gridDim.x) * kRT) {
+    const int rows = static_cast<int>(min(static_cast<long long>(kRT), R - r0));
+    double v0[NT], v1[NT];
+    const int ra = threadIdx.x, rb = threadIdx.x + kRotThreads;
+#pragma unroll
+    for (int l = 0; l < NT; ++l) {
+      v0[l] = (ra < rows) ? __ldg(in + static_cast<long long>(l) * R + r0 + ra) : 0.0;
+      v1[l] = (rb < rows) ? __ldg(in + static_cast<long long>(l) * R + r0 + rb) : 0.0;
+    }
+    __syncthreads();  // Es ready / previous tile stored
+    for (int j = 0; j < k; ++j) {
+      const double* er = Es + j * NT;
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int l = 0; l < NT; ++l) {
+        const double w = er[l];
+        a0 = fma(w, v0[l], a0);
+        a1 = fma(w, v1[l], a1);
+      }
+      Os[ra * k + j] = a0;
+      Os[rb * k + j] = a1;
+    }
+    __syncthreads();
+    double* dst = out + r0 * k;
+    const int cnt = rows * k;
+    for (int e = threadIdx.x; e < cnt; e += blockDim.x) dst[e] = Os[e];
+  }
+}
+
+template <int TN>
+struct Tag { static constexpr int value = TN; };
+
+template <typename F>
+bool dispatch_rot(int n, F&& f) {
+  switch (n) {
+#define CB_CASE(v) case v: f(Tag<v>{}); return true;
+    CB_CASE(1) CB_CASE(2) CB_CASE(3) CB_CASE(4) CB_CASE(5) CB_CASE(6) CB_CASE(7) CB_CASE(8)
+    CB_CASE(9) CB_CASE(10) CB_CASE(11) CB_CASE(12) CB_CASE(13) CB_CASE(14) CB_CASE(15) CB_CASE(16)
+    CB_CASE(17) CB_CASE(18) CB_CASE(19) CB_CASE(20) CB_CASE(21) CB_CASE(22) CB_CASE(23) CB_CASE(24)
+    CB_CASE(25) CB_CASE(26) CB_CASE(27) CB_CASE(28) CB_CASE(29) CB_CASE(30) CB_CASE(31) CB_CASE(32)
+    CB_CASE(33) CB_CASE(34)
+#undef CB_CASE
+    default: return false;
+  }
+}
+
+struct DiagParams {
+  const double* x;
+  const double* W;   // optional (M, n) row-major weights; replaces T_l(x_m) when non-null
+  const double* in;
+  double* out;
+  Status* st;
+  long long M, R;
+  int n;
+  long long sM, sL, sR, oM, oR;
+  int m_fast;  // thread index varies m fastest (input stride along m is 1)
+  int clamp;   // apply clamp_reference semantics to x
+};
+
+__global__ void __launch_bounds__(kAxThreads) contract_diagonal_kernel(DiagParams p) {
+  const long long total = p.M * p.R;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    long long m, r;
+    if (p.m_fast) {
+      m = e % p.M;
+      r = e / p.M;
+    } else {
+      r = e % p.R;
+      m = e / p.R;
+    }
+    const double* src = p.in + m * p.sM + r * p.sR;
+    if (p.W) {
+      const double* w = p.W + m * p.n;
+      double acc = 0.0;
+      for (int l = 0; l < p.n; ++l) acc = fma(__ldg(w + l), src[l * p.sL], acc);
+      p.out[m * p.oM + r * p.oR] = acc;
+      continue;
+    }
+    // only the r == 0 thread of each member reports domain errors (one report per point)
+    const double x = p.clamp ? clamp_ref(__ldg(p.x + m), r == 0 ? p.st : nullptr) : __ldg(p.x + m);
+    const double x2 = 2.0 * x;
+    double t0 = 1.0, t1 = x;
+    double acc = src[0];
+    if (p.n > 1) acc = fma(x, src[p.sL], acc);
+    for (int l = 2; l < p.n; ++l) {
+      const double t2 = fma(x2, t1, -t0);
+      t0 = t1;
+      t1 = t2;
+      acc = fma(t2, src[l * p.sL], acc);
+    }
+    p.out[m * p.oM + r * p.oR] = acc;
+  }
+}
+
+__global__ void basis_matrix_kernel(long long k, const double* x, int size, double* out, Status* st, int clamp) {
+  for (long long j = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; j < k;
+       j += static_cast<long long>(gridDim.x) * blockDim.x) {
+    double v = __ldg(x + j);
+    if (clamp) v = clamp_ref(v, st);
+    cheb_row(v, size, out + j * size, 1);
+  }
+}
+
+__global__ void gather_index_kernel(long long rest, long long count, long long* flat) {
+  const long long total = rest * count;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long m = i / rest, r = i - m * rest;
+    flat[i] = r + rest * (count + 1) * m;
+  }
+}
+
+constexpr int kMaxTakeDims = 12;
+struct TakeParams {
+  int nd_in, nd_out;
+  long long shp_in[kMaxTakeDims], str_in[kMaxTakeDims];
+  long long shp_out[kMaxTakeDims], str_out[kMaxTakeDims];
+  const double* in;
+  const long long* flat;
+  double* out;
+  long long nsel;
+};
+
+__device__ __forceinline__ long long f_to_c(long long f, int nd, const long long* shp, const long long* str) {
+  long long off = 0;
+  for (int d = 0; d < nd; ++d) {
+    const long long q = f / shp[d];
+    off += (f - q * shp[d]) * str[d];
+    f = q;
+  }
+  return off;
+}
+
+__global__ void gather_take_kernel(TakeParams p) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < p.nsel;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long src = f_to_c(p.flat[i], p.nd_in, p.shp_in, p.str_in);
+    const long long dst = f_to_c(i, p.nd_out, p.shp_out, p.str_out);
+    p.out[dst] = p.in[src];
+  }
+}
+
+// derivative_array (S/cheb1d.py:230-249): one row of (rows, L) coefficients per thread.
+__global__ void derivative_kernel(long long rows, int L, const double* in, double* out) {
+  const int n = L - 1;
+  for (long long r = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; r < rows;
+       r += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double* p = in + r * L;
+    double* q = out + r * n;
+    q[n - 1] = 2.0 * n * p[n];
+    if (n >= 2) q[n - 2] = 2.0 * (n - 1) * p[n - 1];
+    for (int l = n - 3; l >= 0; --l) q[l] = q[l + 2] + 2.0 * (l + 1) * p[l + 1];
+    q[0] *= 0.5;
+  }
+}
+
+unsigned grid_for(long long total, int threads) {
+  long long g = (total + threads - 1) / threads;
+  const long long cap = static_cast<long long>(num_sms()) * 32;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return static_cast<unsigned>(g);
+}
+
+}  // namespace
+
+cudaError_t contract_axis(long long A, int n, long long R, long long Q, int k, const double* E, const double* in,
+                          double* out, long long oA, long long oJ, long long oR, cudaStream_t stream) {
+  if (A <= 0 || R <= 0 || Q <= 0 || k <= 0) return cudaSuccess;
+  // fast rotating path
+  if (A == 1 && Q == 1 && oJ == 1 && oR == k && n <= 34) {
+    const size_t smem = sizeof(double) * (((k * n + 1) & ~1) + static_cast<size_t>(kRT) * k);
+    if (smem <= 200 * 1024) {
+      bool done = dispatch_rot(n, [&](auto tag) {
+        constexpr int NT = decltype(tag)::value;
+        ensure_smem_attr(reinterpret_cast<const void*>(rotate_fixed<NT>), 200 * 1024);
+        long long g = (R + kRT - 1) / kRT;
+        const long long cap = static_cast<long long>(num_sms()) * 8;
+        if (g > cap) g = cap;
+        rotate_fixed<NT><<<static_cast<unsigned>(g), kRotThreads, smem, stream>>>(E, in, out, R, k);
+  count_launch();
+      });
+      if (done) return cudaGetLastError();
+    }
+  }
+  AxisParams p{E, in, out, A, R, Q, n, k, oA, oJ, oR, A * k * R * Q};
+  contract_axis_generic<<<grid_for(p.total, kAxThreads), kAxThreads, 0, stream>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t contract_diagonal(long long Mcount, int n, long long R, const double* x, const double* W, int clamp,
+                              const double* in, long long sM, long long sL, long long sR, double* out, long long oM,
+                              long long oR, Status* st, cudaStream_t stream) {
+  if (Mcount <= 0 || R <= 0) return cudaSuccess;
+  DiagParams p{x, W, in, out, st, Mcount, R, n, sM, sL, sR, oM, oR, sM == 1 ? 1 : 0, clamp};
+  contract_diagonal_kernel<<<grid_for(Mcount * R, kAxThreads), kAxThreads, 0, stream>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t derivative(long long rows, int L, const double* in, double* out, cudaStream_t stream) {
+  if (rows <= 0) return cudaSuccess;
+  derivative_kernel<<<grid_for(rows, 128), 128, 0, stream>>>(rows, L, in, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t basis_matrix(long long k, const double* x, int size, double* out, Status* st, int clamp,
+                         cudaStream_t stream) {
+  if (k <= 0) return cudaSuccess;
+  basis_matrix_kernel<<<grid_for(k, 128), 128, 0, stream>>>(k, x, size, out, st, clamp);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t gather_index(long long rest, long long count, long long* flat, cudaStream_t stream) {
+  if (rest * count <= 0) return cudaSuccess;
+  gather_index_kernel<<<grid_for(rest * count, 256), 256, 0, stream>>>(rest, count, flat);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t gather_take_f(int ndim_in, const long long* shape_in, const double* in, long long nsel, const long long* flat,
+                          int ndim_out, const long long* shape_out, double* out, cudaStream_t stream) {
+  if (nsel <= 0) return cudaSuccess;
+  if (ndim_in > kMaxTakeDims || ndim_out > kMaxTakeDims) return cudaErrorInvalidValue;
+  TakeParams p{};
+  p.nd_in = ndim_in;
+  p.nd_out = ndim_out;
+  long long s = 1;
+  for (int d = ndim_in - 1; d >= 0; --d) {
+    p.shp_in[d] = shape_in[d];
+    p.str_in[d] = s;
+    s *= shape_in[d];
+  }
+  s = 1;
+  for (int d = ndim_out - 1; d >= 0; --d) {
+    p.shp_out[d] = shape_out[d];
+    p.str_out[d] = s;
+    s *= shape_out[d];
+  }
+  p.in = in;
+  p.flat = flat;
+  p.out = out;
+  p.nsel = nsel;
+  gather_take_kernel<<<grid_for(nsel, 256), 256, 0, stream>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
+long long eval_grid_work_elems(const EvalLayout& L, const long long* k) {
+  long long dense = 1;
+  for (int d = 0; d < L.J; ++d) dense *= L.n[d];
+  long long mx = dense;
+  long long cur = dense;
+  for (int d = 0; d + 1 < L.J; ++d) {
+    cur = cur / L.n[d] * k[d];
+    if (cur > mx) mx = cur;
+  }
+  return 2 * mx;
+}
+
+cudaError_t eval_grid(const EvalLayout& L, const double* coef, const long long* k, const double* const* E,
+                      double* out, double* work, long long work_elems, cudaStream_t stream) {
+  const int J = L.J;
+  long long dense = 1;
+  for (int d = 0; d < J; ++d) dense *= L.n[d];
+  const long long need = eval_grid_work_elems(L, k);
+  if (work_elems < need) return cudaErrorInvalidValue;
+  double* bufA = work;
+  double* bufB = work + need / 2;
+  const double* cur = coef;
+  if (L.Kp != L.K) {
+    cudaError_t err = cudaMemcpy2DAsync(bufA, sizeof(double) * L.K, coef, sizeof(double) * L.Kp,
+                                        sizeof(double) * L.K, L.R, cudaMemcpyDeviceToDevice, stream);
+    if (err != cudaSuccess) return err;
+    cur = bufA;
+  }
+  long long total = dense;
+  for (int d = 0; d < J; ++d) {
+    const long long R = total / L.n[d];
+    double* dst = (d == J - 1) ? out : ((cur == bufA) ? bufB : bufA);
+    cudaError_t err = contract_axis(1, static_cast<int>(L.n[d]), R, 1, static_cast<int>(k[d]), E[d], cur, dst, 0, 1,
+                                    k[d], stream);
+    if (err != cudaSuccess) return err;
+    total = R * k[d];
+    cur = dst;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace cb

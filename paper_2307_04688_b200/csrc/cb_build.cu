@@ -1,0 +1,434 @@
+// K1: Chebyshev interpolant build (node values -> coefficient tensor) on sm_100a, fp64.
+//
+// Reference: tensor_coeffs S/chebnd.py:162-190 applies the 1-D DCT-I (cheb_transform,
+// S/cheb1d.py:138-170, an rfft of the even extension) along every mode, rotating the axes
+// in between.  Mathematically that is J mode-n products with the n x n matrix
+// M0 = diag(s) B^T diag(w) of S/solver.py:162-171.  Here the mode products are applied to
+// shared-memory tiles that span a GROUP of consecutive modes, so a tensor is read from and
+// written to global memory once per group (1 pass for tensors up to ~12k elements, 2 passes for
+// the J=5/J=6 BASELINE shapes, with the intermediate resident in the 126 MB L2) rather than once
+// per mode.  Each fiber product uses the even/odd fold M0[l, N-k] = (-1)^l M0[l, k], which halves
+// the flops (n/2 FMA per element per mode).
+//
+// Two pass flavours:
+//   contiguous : the group ends with the last tensor mode; a tile is one contiguous block of
+//                prod(n_group) values.  Output may be written in the pitched "eval layout"
+//                (rows of K values padded to Kp) consumed by the K2 evaluator.
+//   strided    : a group of leading/middle modes; a tile is prod(n_group) rows x ct contiguous
+//                inner columns.  Runs in place after the first pass.
+#include "cb_common.cuh"
+#include "cb_kernels.h"
+
+namespace cb {
+
+namespace {
+
+constexpr int kBuildThreads = 256;
+constexpr int kMaxGroup = 4;
+constexpr int kMaxTemplN = 34;   // fiber sizes with a fully unrolled register path
+constexpr int kMaxGenericN = 128;   // degree <= 127 on the generic (non-unrolled) path
+
+struct PassParams {
+  const double* in;
+  double* out;
+  Status* st;
+  int check_finite;
+  int contiguous;
+  int k;                      // modes in the group
+  int n[kMaxGroup];           // their sizes, outer -> inner
+  int sm_stride[kMaxGroup];   // smem stride of each mode
+  int sm_outer[kMaxGroup];    // smem stride of the dim before each mode (ext_i * stride_i)
+  FastDiv fd_inner[kMaxGroup];  // divisor = real element count after mode i (incl. ct)
+  int fibers[kMaxGroup];      // number of fibers for each mode
+  int moff[kMaxGroup];        // offset of each mode's folded matrix in smem
+  int mat_total;              // doubles of folded matrices
+  int tile_elems;             // real elements per tile (incl. ct)
+  int tile_smem;              // smem doubles of the tile (with padding)
+  long long tiles;
+  // contiguous flavour
+  int nlast, nls;             // last mode size and its padded smem extent
+  FastDiv fd_nlast, fd_K;
+  int K, Kp;
+  long long in_tile_stride, out_tile_stride;
+  // strided flavour
+  long long Cn;               // inner extent (contiguous elements per group row)
+  int ct;                     // inner tile width (power of two)
+  int ct_shift;
+  long long ctiles;           // column tiles per outer index
+};
+
+// Folded matrix for a mode of size n: Mf[l][j] for j in [0, H] (H = n/2), row pitch H+1.
+__device__ void fill_folded(double* Mf, int n, int tid, int nthreads) {
+  int N = n - 1, H = n / 2, pitch = H + 1;
+  for (int e = tid; e < n * pitch; e += nthreads) {
+    int l = e / pitch, j = e - l * pitch;
+    Mf[e] = (j <= N) ? transform_entry(l, j, N) : 0.0;
+  }
+}
+
+template <int TN>
+__device__ __forceinline__ void fiber_fixed(double* s, int stride, const double* Mf) {
+  if constexpr (TN == 1) {
+    return;  // degree 0: cheb_transform returns a copy (S/cheb1d.py:163-164)
+  } else {
+    constexpr int N = TN - 1;
+    constexpr int H = TN / 2;
+    constexpr int P = H + 1;
+    double e[H], o[H];
+#pragma unroll
+    for (int k = 0; k < H; ++k) {
+      double a = s[k * stride];
+      double b = s[(N - k) * stride];
+      e[k] = a + b;
+      o[k] = a - b;
+    }
+    double mid = 0.0;
+    if constexpr (TN & 1) mid = s[H * stride];
+#pragma unroll
+    for (int l = 0; l <= N; ++l) {
+      const double* row = Mf + l * P;
+      double acc = 0.0;
+      if ((l & 1) == 0) {
+#pragma unroll
+        for (int k = 0; k < H; ++k) acc = fma(row[k], e[k], acc);
+        if constexpr (TN & 1) acc = fma(row[H], mid, acc);
+      } else {
+#pragma unroll
+        for (int k = 0; k < H; ++k) acc = fma(row[k], o[k], acc);
+      }
+      s[l * stride] = acc;
+    }
+  }
+}
+
+__device__ void fiber_generic(double* s, int stride, const double* Mf, int n) {
+  if (n == 1) return;
+  int N = n - 1, H = n / 2, P = H + 1;
+  double e[kMaxGenericN / 2], o[kMaxGenericN / 2];
+  for (int k = 0; k < H; ++k) {
+    double a = s[k * stride], b = s[(N - k) * stride];
+    e[k] = a + b;
+    o[k] = a - b;
+  }
+  double mid = (n & 1) ? s[H * stride] : 0.0;
+  for (int l = 0; l <= N; ++l) {
+    const double* row = Mf + l * P;
+    double acc = 0.0;
+    if ((l & 1) == 0) {
+      for (int k = 0; k < H; ++k) acc = fma(row[k], e[k], acc);
+      if (n & 1) acc = fma(row[H], mid, acc);
+    } else {
+      for (int k = 0; k < H; ++k) acc = fma(row[k], o[k], acc);
+    }
+    s[l * stride] = acc;
+  }
+}
+
+template <int TN>
+__device__ __forceinline__ void mode_loop_fixed(double* sm, const PassParams& p, int i, const double* Mf) {
+  const int stride = p.sm_stride[i];
+  const int outer = p.sm_outer[i];
+  const bool inner_pad = p.contiguous && (i < p.k - 1);
+  for (int f = threadIdx.x; f < p.fibers[i]; f += blockDim.x) {
+    uint32_t fo, fi;
+    p.fd_inner[i].divmod(static_cast<uint32_t>(f), fo, fi);
+    uint32_t off = fi;
+    if (inner_pad) {
+      uint32_t q, r;
+      p.fd_nlast.divmod(fi, q, r);
+      off = q * p.nls + r;
+    }
+    fiber_fixed<TN>(sm + fo * outer + off, stride, Mf);
+  }
+}
+
+__device__ void mode_loop_generic(double* sm, const PassParams& p, int i, const double* Mf) {
+  const int stride = p.sm_stride[i];
+  const int outer = p.sm_outer[i];
+  const bool inner_pad = p.contiguous && (i < p.k - 1);
+  for (int f = threadIdx.x; f < p.fibers[i]; f += blockDim.x) {
+    uint32_t fo, fi;
+    p.fd_inner[i].divmod(static_cast<uint32_t>(f), fo, fi);
+    uint32_t off = fi;
+    if (inner_pad) {
+      uint32_t q, r;
+      p.fd_nlast.divmod(fi, q, r);
+      off = q * p.nls + r;
+    }
+    fiber_generic(sm + fo * outer + off, stride, Mf, p.n[i]);
+  }
+}
+
+template <int TN>
+struct ModeTag { static constexpr int value = TN; };
+
+template <typename F>
+__device__ __forceinline__ bool dispatch_n(int n, F&& f) {
+  switch (n) {
+#define CB_CASE(v) case v: f(ModeTag<v>{}); return true;
+    CB_CASE(1) CB_CASE(2) CB_CASE(3) CB_CASE(4) CB_CASE(5) CB_CASE(6) CB_CASE(7) CB_CASE(8)
+    CB_CASE(9) CB_CASE(10) CB_CASE(11) CB_CASE(12) CB_CASE(13) CB_CASE(14) CB_CASE(15) CB_CASE(16)
+    CB_CASE(17) CB_CASE(18) CB_CASE(19) CB_CASE(20) CB_CASE(21) CB_CASE(22) CB_CASE(23) CB_CASE(24)
+    CB_CASE(25) CB_CASE(26) CB_CASE(27) CB_CASE(28) CB_CASE(29) CB_CASE(30) CB_CASE(31) CB_CASE(32)
+    CB_CASE(33) CB_CASE(34)
+#undef CB_CASE
+    default: return false;
+  }
+}
+
+__global__ void __launch_bounds__(kBuildThreads) build_pass_kernel(PassParams p) {
+  extern __shared__ __align__(16) double smem[];
+  double* mats = smem;
+  double* tile = smem + ((p.mat_total + 1) & ~1);
+
+  for (int i = 0; i < p.k; ++i) fill_folded(mats + p.moff[i], p.n[i], threadIdx.x, blockDim.x);
+
+  for (long long t = blockIdx.x; t < p.tiles; t += gridDim.x) {
+    __syncthreads();  // previous tile fully stored (and matrices ready on the first tile)
+    // ---------------- load ----------------
+    if (p.contiguous) {
+      const double* src = p.in + t * p.in_tile_stride;
+      for (int e = threadIdx.x; e < p.tile_elems; e += blockDim.x) {
+        double v = __ldg(src + e);
+        if (p.check_finite && !isfinite(v)) atomicAdd(&p.st->nonfinite, 1u);
+        uint32_t q, r;
+        p.fd_nlast.divmod(static_cast<uint32_t>(e), q, r);
+        tile[q * p.nls + r] = v;
+      }
+    } else {
+      long long a = t / p.ctiles;
+      long long c0 = (t - a * p.ctiles) * p.ct;
+      const double* src = p.in + a * (p.tile_elems / p.ct) * p.Cn + c0;
+      for (int e = threadIdx.x; e < p.tile_elems; e += blockDim.x) {
+        int b = e >> p.ct_shift, c = e & (p.ct - 1);
+        double v = 0.0;
+        if (c0 + c < p.Cn) {
+          v = src[static_cast<long long>(b) * p.Cn + c];
+          if (p.check_finite && !isfinite(v)) atomicAdd(&p.st->nonfinite, 1u);
+        }
+        tile[e] = v;
+      }
+    }
+    // ---------------- mode products in shared memory ----------------
+    for (int i = 0; i < p.k; ++i) {
+      __syncthreads();
+      const double* Mf = mats + p.moff[i];
+      bool done = dispatch_n(p.n[i], [&](auto tag) {
+        mode_loop_fixed<decltype(tag)::value>(tile, p, i, Mf);
+      });
+      if (!done) mode_loop_generic(tile, p, i, Mf);
+    }
+    __syncthreads();
+    // ---------------- store ----------------
+    if (p.contiguous) {
+      double* dst = p.out + t * p.out_tile_stride;
+      for (int e = threadIdx.x; e < p.tile_elems; e += blockDim.x) {
+        uint32_t q, r;
+        p.fd_nlast.divmod(static_cast<uint32_t>(e), q, r);
+        double v = tile[q * p.nls + r];
+        uint32_t row, col;
+        p.fd_K.divmod(static_cast<uint32_t>(e), row, col);
+        dst[static_cast<long long>(row) * p.Kp + col] = v;
+      }
+      if (p.Kp > p.K) {
+        int padw = p.Kp - p.K;
+        int rows = p.tile_elems / p.K;
+        for (int z = threadIdx.x; z < rows * padw; z += blockDim.x) {
+          int row = z / padw, col = p.K + (z - row * padw);
+          dst[static_cast<long long>(row) * p.Kp + col] = 0.0;
+        }
+      }
+    } else {
+      long long a = t / p.ctiles;
+      long long c0 = (t - a * p.ctiles) * p.ct;
+      double* dst = p.out + a * (p.tile_elems / p.ct) * p.Cn + c0;
+      for (int e = threadIdx.x; e < p.tile_elems; e += blockDim.x) {
+        int b = e >> p.ct_shift, c = e & (p.ct - 1);
+        if (c0 + c < p.Cn) dst[static_cast<long long>(b) * p.Cn + c] = tile[e];
+      }
+    }
+  }
+}
+
+// Smem budget per tile (doubles).  96 KB keeps two CTAs per SM.
+constexpr int kTileBudget = 12288;
+
+// Fill the group-dependent smem geometry of a pass.
+void finish_geometry(PassParams& p) {
+  // smem extents: contiguous -> dims (n_0..n_{k-1}) with the last padded to odd;
+  //               strided    -> dims (n_0..n_{k-1}, ct) dense.
+  int ext_last_stride;
+  if (p.contiguous) {
+    p.nlast = p.n[p.k - 1];
+    p.nls = (p.nlast % 2 == 0) ? p.nlast + 1 : p.nlast;
+    p.sm_stride[p.k - 1] = 1;
+    p.sm_outer[p.k - 1] = p.nls;
+    ext_last_stride = p.nls;
+  } else {
+    p.nlast = p.n[p.k - 1];
+    p.nls = p.nlast;
+    p.sm_stride[p.k - 1] = p.ct;
+    p.sm_outer[p.k - 1] = p.ct * p.nlast;
+    ext_last_stride = p.ct * p.nlast;
+  }
+  for (int i = p.k - 2; i >= 0; --i) {
+    p.sm_stride[i] = ext_last_stride;
+    p.sm_outer[i] = ext_last_stride * p.n[i];
+    ext_last_stride *= p.n[i];
+  }
+  p.tile_smem = ext_last_stride;
+  long long real = p.contiguous ? 1 : p.ct;
+  for (int i = 0; i < p.k; ++i) real *= p.n[i];
+  p.tile_elems = static_cast<int>(real);
+  for (int i = 0; i < p.k; ++i) {
+    long long inner = p.contiguous ? 1 : p.ct;
+    for (int m = i + 1; m < p.k; ++m) inner *= p.n[m];
+    p.fd_inner[i] = FastDiv(static_cast<uint32_t>(inner));
+    p.fibers[i] = static_cast<int>(real / p.n[i]);
+  }
+  p.fd_nlast = FastDiv(static_cast<uint32_t>(p.nlast));
+  int off = 0;
+  for (int i = 0; i < p.k; ++i) {
+    p.moff[i] = off;
+    off += p.n[i] * (p.n[i] / 2 + 1);
+  }
+  p.mat_total = off;
+}
+
+cudaError_t launch_pass(PassParams& p, cudaStream_t stream) {
+  size_t smem = sizeof(double) * (static_cast<size_t>((p.mat_total + 1) & ~1) + p.tile_smem);
+  ensure_smem_attr(reinterpret_cast<const void*>(build_pass_kernel), 200 * 1024);
+  long long grid = p.tiles;
+  long long cap = static_cast<long long>(num_sms()) * 8;
+  if (grid > cap) grid = cap;
+  if (grid < 1) grid = 1;
+  build_pass_kernel<<<static_cast<unsigned>(grid), kBuildThreads, smem, stream>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// Transform the consecutive axes [a0, a1) of a dense C-order array `shape` (ndim dims).
+// When `evl` is non-null the call is a full tensor build (a0 = 0, a1 = ndim) and the output is
+// written in the eval layout described by evl.
+cudaError_t transform_axes(int ndim, const long long* shape, int a0, int a1, const double* in, double* out,
+                           Status* st, int check_finite, const EvalLayout* evl, cudaStream_t stream) {
+  if (a0 >= a1) {
+    // nothing to transform: plain copy
+    long long total = 1;
+    for (int d = 0; d < ndim; ++d) total *= shape[d];
+    if (in != out) return cudaMemcpyAsync(out, in, sizeof(double) * total, cudaMemcpyDeviceToDevice, stream);
+    return cudaSuccess;
+  }
+  for (int d = a0; d < a1; ++d)
+    if (shape[d] < 1 || shape[d] > kMaxGenericN) return cudaErrorInvalidValue;
+  long long inner = 1;
+  for (int d = a1; d < ndim; ++d) inner *= shape[d];
+  long long outer = 1;
+  for (int d = 0; d < a0; ++d) outer *= shape[d];
+
+  const double* cur_in = in;
+  int hi = a1;  // modes [a0, hi) still to do
+  bool first = true;
+
+  // Pass 1 (contiguous) when the transformed modes are innermost.
+  if (inner == 1) {
+    int g = 0;
+    long long prod = 1;
+    while (hi - g - 1 >= a0) {
+      long long next = prod * shape[hi - g - 1];
+      long long padded = (next / shape[hi - 1]) * (shape[hi - 1] + 1);
+      if (padded > kTileBudget || g >= kMaxGroup) break;
+      prod = next;
+      ++g;
+    }
+    if (evl) {
+      // the contiguous group must cover the q merged modes
+      if (g < evl->q) return cudaErrorInvalidValue;
+    }
+    if (g >= 1) {
+      PassParams p{};
+      p.in = cur_in;
+      p.out = out;
+      p.st = st;
+      p.check_finite = check_finite;
+      p.contiguous = 1;
+      p.k = g;
+      for (int i = 0; i < g; ++i) p.n[i] = static_cast<int>(shape[hi - g + i]);
+      p.ct = 1;
+      finish_geometry(p);
+      long long rest = outer;
+      for (int d = a0; d < hi - g; ++d) rest *= shape[d];
+      p.tiles = rest;
+      p.in_tile_stride = prod;
+      if (evl) {
+        p.K = static_cast<int>(evl->K);
+        p.Kp = static_cast<int>(evl->Kp);
+        p.out_tile_stride = (prod / evl->K) * evl->Kp;
+      } else {
+        p.K = static_cast<int>(prod);
+        p.Kp = p.K;
+        p.out_tile_stride = prod;
+      }
+      p.fd_K = FastDiv(static_cast<uint32_t>(p.K));
+      cudaError_t err = launch_pass(p, stream);
+      if (err != cudaSuccess) return err;
+      cur_in = out;
+      first = false;
+      hi -= g;
+    }
+  } else if (evl) {
+    return cudaErrorInvalidValue;
+  }
+
+  // Remaining modes: strided groups, innermost first, in place on `out`.
+  while (hi > a0) {
+    // inner extent (in the output layout) of the modes after `hi`
+    long long Cn = 1;
+    if (evl) {
+      for (int d = hi; d < ndim - evl->q; ++d) Cn *= shape[d];
+      Cn *= evl->Kp;
+    } else {
+      for (int d = hi; d < ndim; ++d) Cn *= shape[d];
+    }
+    int g = 0;
+    long long prod = 1;
+    while (hi - g - 1 >= a0 && g < kMaxGroup) {
+      long long next = prod * shape[hi - g - 1];
+      if (next * 4 > kTileBudget && g >= 1) break;
+      prod = next;
+      ++g;
+    }
+    int ct = 32;
+    while (ct > 1 && (prod * ct > kTileBudget || ct / 2 >= Cn)) ct >>= 1;
+    PassParams p{};
+    p.in = cur_in;
+    p.out = out;
+    p.st = st;
+    p.check_finite = first ? check_finite : 0;
+    p.contiguous = 0;
+    p.k = g;
+    for (int i = 0; i < g; ++i) p.n[i] = static_cast<int>(shape[hi - g + i]);
+    p.ct = ct;
+    p.ct_shift = 0;
+    while ((1 << p.ct_shift) < ct) ++p.ct_shift;
+    p.Cn = Cn;
+    finish_geometry(p);
+    long long A = outer;
+    for (int d = a0; d < hi - g; ++d) A *= shape[d];
+    p.ctiles = (Cn + ct - 1) / ct;
+    p.tiles = A * p.ctiles;
+    cudaError_t err = launch_pass(p, stream);
+    if (err != cudaSuccess) return err;
+    cur_in = out;
+    first = false;
+    hi -= g;
+  }
+  if (evl && evl->R8 > evl->R) {
+    return cudaMemsetAsync(out + evl->R * evl->Kp, 0, sizeof(double) * (evl->R8 - evl->R) * evl->Kp, stream);
+  }
+  return cudaSuccess;
+}
+
+}  // namespace cb

@@ -1,0 +1,378 @@
+// C ABI (include/chebnash_b200.h): argument validation, layout planning, stream plumbing and
+// the device-resident time loop.  All numerics run in the kernels of cb_build.cu, cb_eval.cu and
+// cb_axis.cu.
+#include <cstdio>
+#include <cstring>
+#include <atomic>
+#include <mutex>
+#include <string>
+#include "../../include/chebnash_b200.h"
+#include "cb_common.cuh"
+#include "cb_kernels.h"
+
+namespace cb {
+
+namespace {
+thread_local std::string g_last_error;
+std::mutex g_attr_mutex;
+constexpr int kMaxDevices = 64;
+struct AttrEntry {
+  const void* func;
+  int bytes;
+};
+AttrEntry g_attr[kMaxDevices][64];
+int g_attr_n[kMaxDevices];
+int g_sms[kMaxDevices];
+}  // namespace
+
+void ensure_smem_attr(const void* func, int bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) return;
+  std::lock_guard<std::mutex> lock(g_attr_mutex);
+  for (int i = 0; i < g_attr_n[dev]; ++i)
+    if (g_attr[dev][i].func == func && g_attr[dev][i].bytes >= bytes) return;
+  cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (g_attr_n[dev] < 64) g_attr[dev][g_attr_n[dev]++] = {func, bytes};
+}
+
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+int num_sms() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) return 148;
+  if (!g_sms[dev]) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    g_sms[dev] = sms > 0 ? sms : 148;
+  }
+  return g_sms[dev];
+}
+
+}  // namespace cb
+
+using namespace cb;
+
+static int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+static int cuda_fail(cudaError_t err, const char* where) {
+  std::string m = std::string(where) + ": " + cudaGetErrorName(err) + ": " + cudaGetErrorString(err);
+  return fail(CB_ECUDA, m);
+}
+
+#define CB_CUDA(call, where)                      \
+  do {                                            \
+    cudaError_t e_ = (call);                      \
+    if (e_ != cudaSuccess) return cuda_fail(e_, where); \
+  } while (0)
+
+static int check_dims(int J, const int64_t* n, const char* fn) {
+  if (J < 1 || J > kMaxDims) return fail(CB_EINVAL, std::string(fn) + ": number of modes must be in [1, 8]");
+  if (!n) return fail(CB_EINVAL, std::string(fn) + ": null size array");
+  long long total = 1;
+  for (int d = 0; d < J; ++d) {
+    if (n[d] < 1) return fail(CB_EINVAL, std::string(fn) + ": mode sizes must be >= 1");
+    if (n[d] > 128) return fail(CB_EINVAL, std::string(fn) + ": mode size above 128 (degree 127) is not supported");
+    total *= n[d];
+    if (total > (1LL << 31)) return fail(CB_EINVAL, std::string(fn) + ": tensor larger than 2^31 elements");
+  }
+  return CB_OK;
+}
+
+static EvalLayout layout_of(int J, const int64_t* n) {
+  long long nn[kMaxDims];
+  for (int d = 0; d < J; ++d) nn[d] = n[d];
+  return make_eval_layout(J, nn);
+}
+
+extern "C" {
+
+int cb_abi_version(void) { return CB_ABI_VERSION; }
+
+const char* cb_last_error(void) { return g_last_error.c_str(); }
+
+int64_t cb_kernel_launches(void) { return launch_count(); }
+
+int cb_runtime_info(int* device_count, int* sm_count, int* cc_major, int* cc_minor) {
+  int cnt = 0;
+  if (cudaGetDeviceCount(&cnt) != cudaSuccess) {
+    cudaGetLastError();
+    cnt = 0;
+  }
+  if (device_count) *device_count = cnt;
+  if (sm_count) *sm_count = 0;
+  if (cc_major) *cc_major = 0;
+  if (cc_minor) *cc_minor = 0;
+  if (cnt > 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (sm_count) cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, dev);
+    if (cc_major) cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (cc_minor) cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
+  }
+  return CB_OK;
+}
+
+int cb_eval_layout(int J, const int64_t* n, int64_t* out6) {
+  int rc = check_dims(J, n, "cb_eval_layout");
+  if (rc) return rc;
+  EvalLayout L = layout_of(J, n);
+  out6[0] = L.q;
+  out6[1] = L.R;
+  out6[2] = L.R8;
+  out6[3] = L.K;
+  out6[4] = L.Kp;
+  out6[5] = L.elems();
+  return CB_OK;
+}
+
+int cb_pack_eval(int J, const int64_t* n, const double* d_dense, double* d_eval, void* stream) {
+  int rc = check_dims(J, n, "cb_pack_eval");
+  if (rc) return rc;
+  EvalLayout L = layout_of(J, n);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (L.Kp != L.K || L.R8 != L.R) CB_CUDA(cudaMemsetAsync(d_eval, 0, sizeof(double) * L.elems(), s), "cb_pack_eval");
+  CB_CUDA(cudaMemcpy2DAsync(d_eval, sizeof(double) * L.Kp, d_dense, sizeof(double) * L.K, sizeof(double) * L.K, L.R,
+                            cudaMemcpyDeviceToDevice, s),
+          "cb_pack_eval");
+  return CB_OK;
+}
+
+int cb_unpack_eval(int J, const int64_t* n, const double* d_eval, double* d_dense, void* stream) {
+  int rc = check_dims(J, n, "cb_unpack_eval");
+  if (rc) return rc;
+  EvalLayout L = layout_of(J, n);
+  CB_CUDA(cudaMemcpy2DAsync(d_dense, sizeof(double) * L.K, d_eval, sizeof(double) * L.Kp, sizeof(double) * L.K, L.R,
+                            cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)),
+          "cb_unpack_eval");
+  return CB_OK;
+}
+
+int cb_tensor_coeffs(int J, const int64_t* n, const double* d_samples, double* d_coef, void* d_status, void* stream) {
+  int rc = check_dims(J, n, "cb_tensor_coeffs");
+  if (rc) return rc;
+  EvalLayout L = layout_of(J, n);
+  long long shape[kMaxDims];
+  for (int d = 0; d < J; ++d) shape[d] = n[d];
+  CB_CUDA(transform_axes(J, shape, 0, J, d_samples, d_coef, static_cast<Status*>(d_status), 1, &L,
+                         static_cast<cudaStream_t>(stream)),
+          "cb_tensor_coeffs");
+  return CB_OK;
+}
+
+int cb_transform_axes(int ndim, const int64_t* shape, int a0, int a1, const double* d_in, double* d_out,
+                      void* d_status, int check_finite, void* stream) {
+  if (ndim < 1 || ndim > 16 || a0 < 0 || a1 > ndim || a0 > a1)
+    return fail(CB_EINVAL, "cb_transform_axes: bad axes");
+  long long shp[16];
+  long long total = 1;
+  for (int d = 0; d < ndim; ++d) {
+    if (shape[d] < 1) return fail(CB_EINVAL, "cb_transform_axes: empty axis");
+    shp[d] = shape[d];
+    total *= shape[d];
+    if (total > (1LL << 31)) return fail(CB_EINVAL, "cb_transform_axes: array larger than 2^31 elements");
+  }
+  for (int d = a0; d < a1; ++d)
+    if (shape[d] > 128) return fail(CB_EINVAL, "cb_transform_axes: axis longer than 128 (degree 127) not supported");
+  CB_CUDA(transform_axes(ndim, shp, a0, a1, d_in, d_out, static_cast<Status*>(d_status), check_finite, nullptr,
+                         static_cast<cudaStream_t>(stream)),
+          "cb_transform_axes");
+  return CB_OK;
+}
+
+int cb_eval_points(int J, const int64_t* n, const double* d_coef, int64_t M, const double* d_points, double* d_out,
+                   void* d_status, int flags, void* stream) {
+  int rc = check_dims(J, n, "cb_eval_points");
+  if (rc) return rc;
+  if (M < 0) return fail(CB_EINVAL, "cb_eval_points: negative point count");
+  EvalLayout L = layout_of(J, n);
+  CB_CUDA(eval_points(L, d_coef, M, d_points, nullptr, d_out, static_cast<Status*>(d_status), flags & 1,
+                      static_cast<cudaStream_t>(stream)),
+          "cb_eval_points");
+  return CB_OK;
+}
+
+static int fill_advect(int J, const double* A, double dt, const double* lo, const double* hi, int source,
+                       AdvectSpec& adv) {
+  std::memset(&adv, 0, sizeof(adv));
+  for (int i = 0; i < J * J; ++i) adv.A[i] = A[i];
+  adv.dt = dt;
+  for (int d = 0; d < J; ++d) {
+    if (!(hi[d] > lo[d])) return fail(CB_EINVAL, "interval must satisfy a < b");
+    adv.lo[d] = lo[d];
+    adv.hi[d] = hi[d];
+  }
+  adv.source = source;
+  return CB_OK;
+}
+
+int cb_eval_advected(int J, const int64_t* n, const double* d_coef, int64_t node_begin, int64_t count,
+                     const double* A, double dt, const double* lo, const double* hi, int source, double* d_out,
+                     void* stream) {
+  int rc = check_dims(J, n, "cb_eval_advected");
+  if (rc) return rc;
+  for (int d = 0; d < J; ++d)
+    if (n[d] > 64) return fail(CB_EINVAL, "cb_eval_advected: mode size above 64 not supported");
+  EvalLayout L = layout_of(J, n);
+  AdvectSpec adv;
+  rc = fill_advect(J, A, dt, lo, hi, source, adv);
+  if (rc) return rc;
+  adv.node_begin = node_begin;
+  CB_CUDA(eval_points(L, d_coef, count, nullptr, &adv, d_out, nullptr, 0, static_cast<cudaStream_t>(stream)),
+          "cb_eval_advected");
+  return CB_OK;
+}
+
+static cudaError_t loop_step(const EvalLayout& L, const long long* shape, const AdvectSpec& adv, const double* vin,
+                             double* vout, double* coef, Status* st, long long N, cudaStream_t s) {
+  cudaError_t e = transform_axes(L.J, shape, 0, L.J, vin, coef, st, 1, &L, s);
+  if (e != cudaSuccess) return e;
+  return eval_points(L, coef, N, nullptr, &adv, vout, nullptr, 0, s);
+}
+
+int cb_advect_loop(int J, const int64_t* n, double* d_values, double* d_tmp, double* d_coef, int steps,
+                   const double* A, double dt, const double* lo, const double* hi, void* d_status, int use_graph,
+                   void* stream) {
+  int rc = check_dims(J, n, "cb_advect_loop");
+  if (rc) return rc;
+  for (int d = 0; d < J; ++d)
+    if (n[d] > 64) return fail(CB_EINVAL, "cb_advect_loop: mode size above 64 not supported");
+  if (steps < 0) return fail(CB_EINVAL, "cb_advect_loop: negative step count");
+  EvalLayout L = layout_of(J, n);
+  AdvectSpec adv;
+  rc = fill_advect(J, A, dt, lo, hi, 1, adv);
+  if (rc) return rc;
+  adv.node_begin = 0;
+  long long shape[kMaxDims];
+  long long N = 1;
+  for (int d = 0; d < J; ++d) {
+    shape[d] = n[d];
+    N *= n[d];
+  }
+  cudaStream_t user = static_cast<cudaStream_t>(stream);
+  Status* st = static_cast<Status*>(d_status);
+  if (steps == 0) return CB_OK;
+  const int pairs = steps / 2;
+  if (!use_graph || pairs < 2) {
+    for (int s = 0; s < pairs; ++s) {
+      CB_CUDA(loop_step(L, shape, adv, d_values, d_tmp, d_coef, st, N, user), "cb_advect_loop");
+      CB_CUDA(loop_step(L, shape, adv, d_tmp, d_values, d_coef, st, N, user), "cb_advect_loop");
+    }
+  } else {
+    // Capture one step pair on a private stream (the caller's stream may be the legacy default
+    // stream, which cannot be captured), then replay it; ordered after / before `user` by events.
+    cudaStream_t cs;
+    CB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "cb_advect_loop: stream");
+    cudaEvent_t ev;
+    CB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cb_advect_loop: event");
+    CB_CUDA(cudaEventRecord(ev, user), "cb_advect_loop: record");
+    CB_CUDA(cudaStreamWaitEvent(cs, ev, 0), "cb_advect_loop: wait");
+    cudaGraph_t graph;
+    cudaGraphExec_t exec;
+    CB_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "cb_advect_loop: capture");
+    cudaError_t e1 = loop_step(L, shape, adv, d_values, d_tmp, d_coef, st, N, cs);
+    cudaError_t e2 = loop_step(L, shape, adv, d_tmp, d_values, d_coef, st, N, cs);
+    cudaError_t e3 = cudaStreamEndCapture(cs, &graph);
+    if (e1 != cudaSuccess) return cuda_fail(e1, "cb_advect_loop: capture step");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "cb_advect_loop: capture step");
+    if (e3 != cudaSuccess) return cuda_fail(e3, "cb_advect_loop: end capture");
+    CB_CUDA(cudaGraphInstantiate(&exec, graph, 0), "cb_advect_loop: instantiate");
+    for (int s = 0; s < pairs; ++s) CB_CUDA(cudaGraphLaunch(exec, cs), "cb_advect_loop: launch");
+    CB_CUDA(cudaEventRecord(ev, cs), "cb_advect_loop: record");
+    CB_CUDA(cudaStreamWaitEvent(user, ev, 0), "cb_advect_loop: wait");
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    cudaEventDestroy(ev);
+    cudaStreamDestroy(cs);  // destruction is deferred until the stream's work completes
+  }
+  if (steps & 1) {
+    CB_CUDA(loop_step(L, shape, adv, d_values, d_tmp, d_coef, st, N, user), "cb_advect_loop");
+    CB_CUDA(cudaMemcpyAsync(d_values, d_tmp, sizeof(double) * N, cudaMemcpyDeviceToDevice, user),
+            "cb_advect_loop: copy");
+  }
+  return CB_OK;
+}
+
+int cb_contract_axis(int64_t A, int n, int64_t R, int64_t Q, int k, const double* d_E, const double* d_in,
+                     double* d_out, int64_t oA, int64_t oJ, int64_t oR, void* stream) {
+  if (A < 0 || n < 1 || R < 0 || Q < 0 || k < 0) return fail(CB_EINVAL, "cb_contract_axis: bad sizes");
+  CB_CUDA(contract_axis(A, n, R, Q, k, d_E, d_in, d_out, oA, oJ, oR, static_cast<cudaStream_t>(stream)),
+          "cb_contract_axis");
+  return CB_OK;
+}
+
+int cb_contract_diagonal(int64_t M, int n, int64_t R, const double* d_x, const double* d_W, int clamp,
+                         const double* d_in, int64_t sM, int64_t sL, int64_t sR, double* d_out, int64_t oM, int64_t oR,
+                         void* d_status, void* stream) {
+  if (M < 0 || n < 1 || R < 0) return fail(CB_EINVAL, "cb_contract_diagonal: bad sizes");
+  if (!d_x && !d_W) return fail(CB_EINVAL, "cb_contract_diagonal: need points or weights");
+  CB_CUDA(contract_diagonal(M, n, R, d_x, d_W, clamp, d_in, sM, sL, sR, d_out, oM, oR, static_cast<Status*>(d_status),
+                            static_cast<cudaStream_t>(stream)),
+          "cb_contract_diagonal");
+  return CB_OK;
+}
+
+int cb_derivative(int64_t rows, int L, const double* d_in, double* d_out, void* stream) {
+  if (rows < 0 || L < 2) return fail(CB_EINVAL, "need degree >= 1 to differentiate");
+  CB_CUDA(derivative(rows, L, d_in, d_out, static_cast<cudaStream_t>(stream)), "cb_derivative");
+  return CB_OK;
+}
+
+int cb_basis_matrix(int64_t k, const double* d_x, int size, double* d_out, void* d_status, int clamp, void* stream) {
+  if (k < 0 || size < 1) return fail(CB_EINVAL, "cb_basis_matrix: bad sizes");
+  CB_CUDA(basis_matrix(k, d_x, size, d_out, static_cast<Status*>(d_status), clamp, static_cast<cudaStream_t>(stream)),
+          "cb_basis_matrix");
+  return CB_OK;
+}
+
+int cb_gather_index(int64_t rest, int64_t count, int64_t* d_flat, void* stream) {
+  if (rest < 1 || count < 1) return fail(CB_EINVAL, "cb_gather_index: bad sizes");
+  CB_CUDA(gather_index(rest, count, reinterpret_cast<long long*>(d_flat), static_cast<cudaStream_t>(stream)),
+          "cb_gather_index");
+  return CB_OK;
+}
+
+int cb_gather_take(int ndim_in, const int64_t* shape_in, const double* d_in, int64_t nsel, const int64_t* d_flat,
+                   int ndim_out, const int64_t* shape_out, double* d_out, void* stream) {
+  if (ndim_in < 1 || ndim_out < 1) return fail(CB_EINVAL, "cb_gather_take: bad ranks");
+  long long si[16], so[16];
+  if (ndim_in > 12 || ndim_out > 12) return fail(CB_EINVAL, "cb_gather_take: rank above 12");
+  for (int d = 0; d < ndim_in; ++d) si[d] = shape_in[d];
+  for (int d = 0; d < ndim_out; ++d) so[d] = shape_out[d];
+  CB_CUDA(gather_take_f(ndim_in, si, d_in, nsel, reinterpret_cast<const long long*>(d_flat), ndim_out, so, d_out,
+                        static_cast<cudaStream_t>(stream)),
+          "cb_gather_take");
+  return CB_OK;
+}
+
+int64_t cb_eval_grid_workspace(int J, const int64_t* n, const int64_t* k) {
+  if (check_dims(J, n, "cb_eval_grid_workspace")) return -1;
+  EvalLayout L = layout_of(J, n);
+  long long kk[kMaxDims];
+  for (int d = 0; d < J; ++d) kk[d] = k[d];
+  return eval_grid_work_elems(L, kk);
+}
+
+int cb_eval_grid(int J, const int64_t* n, const double* d_coef, const int64_t* k, const double* const* d_E,
+                 double* d_out, double* d_work, int64_t work_elems, void* stream) {
+  int rc = check_dims(J, n, "cb_eval_grid");
+  if (rc) return rc;
+  long long kk[kMaxDims];
+  for (int d = 0; d < J; ++d) {
+    if (k[d] < 1) return fail(CB_EINVAL, "cb_eval_grid: empty target axis");
+    kk[d] = k[d];
+  }
+  EvalLayout L = layout_of(J, n);
+  if (work_elems < eval_grid_work_elems(L, kk)) return fail(CB_EINVAL, "cb_eval_grid: workspace too small");
+  CB_CUDA(eval_grid(L, d_coef, kk, d_E, d_out, d_work, work_elems, static_cast<cudaStream_t>(stream)),
+          "cb_eval_grid");
+  return CB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,66 @@
+// Internal (C++) entry points shared between the kernel translation units and the C-ABI layer.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "cb_common.cuh"
+
+namespace cb {
+
+// Eval layout of a J-mode coefficient tensor: the trailing q modes merged into K columns
+// (padded to Kp, a multiple of 4), the leading J-q modes into R rows (padded to R8, a multiple
+// of 8).  See cb_common.cuh and DESIGN.md §3.
+struct EvalLayout {
+  int J;
+  long long n[kMaxDims];
+  int q;
+  long long R, R8, K, Kp;
+  long long elems() const { return R8 * Kp; }
+};
+
+// Choose q (1..J) maximising the DMMA tile efficiency R*K / (R8*Kp) subject to the build's
+// contiguous-tile budget; ties -> smaller q.
+EvalLayout make_eval_layout(int J, const long long* n);
+
+// Per-device one-time cudaFuncSetAttribute(MaxDynamicSharedMemorySize).
+void ensure_smem_attr(const void* func, int bytes);
+int num_sms();
+// Process-wide count of kernels launched by this library (reported as gpu_launches by bench.py).
+void count_launch();
+long long launch_count();
+
+// K1 build / generic axis transform (cb_build.cu).
+cudaError_t transform_axes(int ndim, const long long* shape, int a0, int a1, const double* in, double* out,
+                           Status* st, int check_finite, const EvalLayout* evl, cudaStream_t stream);
+
+// K2 scattered evaluator (cb_eval.cu).
+struct AdvectSpec {
+  long long node_begin;     // first flat node index (C order) evaluated by this call
+  double A[kMaxDims * kMaxDims];  // drift g(x) = A x (row-major J x J), in interval units
+  double dt;
+  double lo[kMaxDims], hi[kMaxDims];  // state box per dim (the grid basis interval)
+  int source;               // subtract dt*|x|^2 of the (unclipped) node
+};
+cudaError_t eval_points(const EvalLayout& L, const double* coef, long long M, const double* points,
+                        const AdvectSpec* adv, double* out, Status* st, int force_generic, cudaStream_t stream);
+
+// K3 / stack contractions (cb_axis.cu).
+//   in  : dense (A, n, R, Q) ;  E : (k, n) row-major ;  out[a*oA + j*oJ + r*oR + q] .
+cudaError_t contract_axis(long long A, int n, long long R, long long Q, int k, const double* E, const double* in,
+                          double* out, long long oA, long long oJ, long long oR, cudaStream_t stream);
+//   out[m*oM + r*oR] = sum_l T_l(x_m) in[m*sM + l*sL + r*sR]   (x_m clamped, status checked)
+//   (W non-null: weights W[m*n + l] replace T_l(x_m); clamp: apply clamp_reference to x)
+cudaError_t contract_diagonal(long long Mcount, int n, long long R, const double* x, const double* W, int clamp,
+                              const double* in, long long sM, long long sL, long long sR, double* out, long long oM,
+                              long long oR, Status* st, cudaStream_t stream);
+cudaError_t derivative(long long rows, int L, const double* in, double* out, cudaStream_t stream);
+cudaError_t basis_matrix(long long k, const double* x, int size, double* out, Status* st, int clamp,
+                         cudaStream_t stream);
+cudaError_t gather_index(long long rest, long long count, long long* flat, cudaStream_t stream);
+cudaError_t gather_take_f(int ndim_in, const long long* shape_in, const double* in, long long nsel, const long long* flat,
+                          int ndim_out, const long long* shape_out, double* out, cudaStream_t stream);
+// eval_grid: J successive rotating mode products with k_j x n_j evaluation matrices.
+cudaError_t eval_grid(const EvalLayout& L, const double* coef, const long long* k, const double* const* E,
+                      double* out, double* work, long long work_elems, cudaStream_t stream);
+long long eval_grid_work_elems(const EvalLayout& L, const long long* k);
+
+}  // namespace cb

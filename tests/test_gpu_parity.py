@@ -1,0 +1,283 @@
+"""GPU parity: the CUDA path (through the C ABI / Python shim) against the CPU oracle
+(oracle/cheb_oracle.py, pinned to the reference in test_oracle_golden.py) on the same seeded inputs.
+
+Tolerance (north star, BASELINE.json): fp64 allclose with rtol = 1e-12 and atol = 1e-11 — summation
+order differs from numpy's pocketfft / OpenBLAS, so pure 1e-12 relative is not meaningful where
+|V| is tiny.  Integer / index work (gather indices) is compared exactly.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2307_04688_b200 as cn
+from oracle import cheb_oracle as orc
+from paper_2307_04688_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+RTOL, ATOL = 1e-12, 1e-11
+
+
+def close(got, ref, rtol=RTOL, atol=ATOL):
+    np.testing.assert_allclose(np.asarray(got), np.asarray(ref), rtol=rtol, atol=atol)
+
+
+def bases_for(J, n, a=0.0, b=1.0):
+    return [cn.make_basis(n - 1, a, b)] * J
+
+
+# ------------------------------------------------------------------------------------------------
+# K1 build
+# ------------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("cfg", ["1", "2", "3", "4", "5a"])
+def test_build_baseline_shapes(cuda, cfg):
+    w = workloads.make(cfg, M=16)
+    t = cn.tensor_coeffs(w.values, bases_for(w.J, w.n))
+    close(t.coefficients, orc.tensor_coeffs(w.values))
+
+
+@pytest.mark.parametrize("shape", [(1,), (2,), (7,), (34,), (65,), (3, 1), (1, 5), (4, 3), (16, 2), (5, 6, 7),
+                                   (2, 2, 2, 2), (3, 4, 5, 6), (8, 9, 10), (33, 33), (2, 3, 2, 3, 2, 3),
+                                   (3, 3, 3, 3, 3, 3, 3, 3), (12, 12, 12), (40, 41)])
+def test_build_ragged_shapes(cuda, shape):
+    rng = np.random.default_rng(abs(hash(shape)) % 2**32)
+    s = rng.standard_normal(shape)
+    bases = [cn.make_basis(d - 1, -1.0, 1.0) for d in shape]
+    close(cn.tensor_coeffs(s, bases).coefficients, orc.tensor_coeffs(s))
+
+
+def test_transform_matches_direct_sum_all_degrees(cuda):
+    rng = np.random.default_rng(23)
+    for n in range(1, 65):
+        s = rng.standard_normal(n + 1)
+        c = cn.coeffs_from_samples(s, cn.make_basis(n, -1.0, 1.0)).coefficients
+        np.testing.assert_allclose(c, orc.direct_transform(s), atol=1e-12)
+
+
+def test_cheb_transform_axis(cuda):
+    rng = np.random.default_rng(7)
+    block = rng.standard_normal((9, 5, 4))
+    for axis in range(3):
+        close(cn.cheb_transform(block, axis=axis), orc.cheb_transform(block, axis=axis))
+
+
+def test_build_rejects_nonfinite(cuda):
+    s = np.ones((4, 4))
+    s[2, 1] = np.nan
+    with pytest.raises(ValueError, match="finite"):
+        cn.tensor_coeffs(s, bases_for(2, 4))
+
+
+def test_stack_coeffs(cuda):
+    rng = np.random.default_rng(30)
+    bases = (cn.make_basis(3, -1.0, 1.0), cn.make_basis(4, -1.0, 1.0))
+    samples = rng.standard_normal((4, 5, 6))
+    st = cn.stack_coeffs(samples, bases)
+    assert st.count == 6
+    close(st.coefficients, orc.stack_coeffs(samples))
+
+
+# ------------------------------------------------------------------------------------------------
+# K2 scattered evaluation
+# ------------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("cfg,M", [("1", 65536), ("2", 20000), ("3", 4096), ("4", 2048), ("5a", 512)])
+def test_eval_points_baseline_shapes(cuda, cfg, M):
+    if cfg == "3":
+        w = workloads.make("3")
+        T, _ = orc.advect_points(w.values.shape, w.A, w.dt)
+        pts = T[:M]
+    elif cfg == "5a":
+        w = workloads.make("5a")
+        pts = 2.0 * np.random.default_rng(5).random((M, 6)) - 1.0
+    else:
+        w = workloads.make(cfg, M=M)
+        pts = w.points
+    t = cn.tensor_coeffs(w.values, bases_for(w.J, w.n))
+    ref_c = orc.tensor_coeffs(w.values)
+    got = cn.eval_points(t, pts)
+    close(got, orc.eval_points(ref_c, pts))
+
+
+@pytest.mark.parametrize("shape", [(5,), (17,), (3, 4), (17, 17), (2, 9, 3), (6, 1, 5), (1, 1, 1), (9, 9, 9, 9),
+                                   (4, 3, 5, 2, 3), (3, 3, 3, 3, 3, 3), (2, 2, 2, 2, 2, 2, 2, 2), (33, 33, 33)])
+@pytest.mark.parametrize("generic", [False, True])
+def test_eval_points_ragged(cuda, shape, generic):
+    rng = np.random.default_rng(len(shape) * 100 + sum(shape))
+    coef = rng.standard_normal(shape)
+    J = len(shape)
+    t = cn.CoefTensor([cn.make_basis(d - 1, -1.0, 1.0) for d in shape], coef)
+    M = 3000
+    pts = rng.uniform(-1.0, 1.0, (M, J))
+    pts[:5] = np.sign(pts[:5])  # exact endpoints
+    from paper_2307_04688_b200 import _lib
+    from paper_2307_04688_b200.chebnd import _eval_points_device
+
+    got = _lib.to_host(_eval_points_device(shape, t.device_coefficients, _lib.to_device(pts), force_generic=generic))
+    ref = orc.eval_points(coef, pts)
+    scale = max(1.0, float(np.abs(coef).sum()))
+    close(got, ref, atol=1e-13 * scale)
+
+
+def test_eval_points_matches_eval_full(cuda):
+    rng = np.random.default_rng(43)
+    coef = rng.standard_normal((4, 5, 3))
+    t = cn.CoefTensor([cn.make_basis(d - 1, -1.0, 1.0) for d in coef.shape], coef)
+    pts = rng.uniform(-1, 1, (20, 3))
+    got = cn.eval_points(t, pts)
+    for i in range(20):
+        assert got[i] == pytest.approx(orc.eval_full(coef, pts[i]), abs=1e-12)
+        assert cn.eval_full(t, pts[i]) == pytest.approx(orc.eval_full(coef, pts[i]), abs=1e-12)
+
+
+def test_eval_points_clamp_semantics(cuda):
+    t = cn.CoefTensor([cn.make_basis(1, -1.0, 1.0)] * 2, np.array([[1.0, 2.0], [3.0, 4.0]]))
+    ok = cn.eval_points(t, np.array([[1.0 + 1e-13, -1.0 - 5e-13]]))
+    close(ok, [orc.eval_full(t.coefficients, [1.0, -1.0])])
+    with pytest.raises(ValueError, match="beyond tolerance"):
+        cn.eval_points(t, np.array([[0.0, 1.0 + 1e-9]]))
+    with pytest.raises(ValueError, match="finite"):
+        cn.eval_points(t, np.array([[np.nan, 0.0]]))
+    with pytest.raises(ValueError):
+        cn.eval_full(t, [0.1, 0.2, 0.3])
+
+
+def test_eval_points_shard_bitwise_invariance(cuda):
+    """Any contiguous sub-batch gives bit-identical values (multi-GPU point sharding contract)."""
+    w = workloads.make("2", M=8192)
+    t = cn.tensor_coeffs(w.values, bases_for(w.J, w.n))
+    full = cn.eval_points(t, w.points)
+    for a, b in ((0, 4096), (4096, 8192), (17, 3000), (8000, 8192)):
+        part = cn.eval_points(t, w.points[a:b])
+        assert np.array_equal(part, full[a:b]), (a, b, float(np.abs(part - full[a:b]).max()))
+
+
+def test_polynomial_exactness(cuda):
+    # T/test_chebnd.py:355-368 (seed 46): exact for polynomials of the basis degrees
+    rng = np.random.default_rng(46)
+    degrees = (3, 2, 4)
+    bases = tuple(cn.make_basis(n, -1.0, 1.0) for n in degrees)
+    mono = rng.standard_normal(tuple(d + 1 for d in degrees))
+    grids = np.meshgrid(*(b.nodes for b in bases), indexing="ij")
+    samples = np.polynomial.polynomial.polyval3d(*grids, mono)
+    t = cn.tensor_coeffs(samples, bases)
+    pts = rng.uniform(-1, 1, (100, 3))
+    close(cn.eval_points(t, pts), np.polynomial.polynomial.polyval3d(*pts.T, mono), rtol=0, atol=1e-10)
+
+
+# ------------------------------------------------------------------------------------------------
+# axis / stack / gather API
+# ------------------------------------------------------------------------------------------------
+
+def test_eval_axis_tensor_and_stack(cuda):
+    rng = np.random.default_rng(35)
+    coef = rng.standard_normal((5, 4, 3))
+    t = cn.CoefTensor([cn.make_basis(d - 1, -1.0, 1.0) for d in coef.shape], coef)
+    pts = rng.uniform(-1, 1, 7)
+    close(cn.eval_axis(t, pts), orc.eval_axis(coef, pts))
+    sc = rng.standard_normal((4, 3, 6))
+    st = cn.TensorStack([cn.make_basis(3, -1, 1), cn.make_basis(2, -1, 1)], sc)
+    close(cn.eval_axis(st, pts), orc.eval_axis_stack(sc, pts))
+    with pytest.raises(ValueError):
+        cn.eval_axis(t, [])
+    with pytest.raises(ValueError):
+        cn.eval_axis(t, [1.5])
+
+
+def test_diagonal_batch_and_gather(cuda):
+    rng = np.random.default_rng(39)
+    sc = rng.standard_normal((5, 3, 4, 6))
+    bases = [cn.make_basis(d - 1, -1, 1) for d in sc.shape[:-1]]
+    st = cn.TensorStack(bases, sc)
+    pts = rng.uniform(-1, 1, 6)
+    g = cn.make_gather_index(sc.shape[:-1], 6)
+    assert np.array_equal(g.flat, orc.gather_index(sc.shape[:-1], 6))
+    direct = cn.eval_diagonal_batch(st, pts, g)
+    close(direct.coefficients, orc.eval_diagonal(sc, pts))
+    gathered = g.take(cn.eval_axis(st, pts))
+    close(gathered, direct.coefficients)
+    with pytest.raises(ValueError):
+        cn.eval_diagonal_batch(st, np.zeros(5), g)
+    with pytest.raises(ValueError):
+        cn.eval_diagonal_batch(st, pts, cn.make_gather_index((99, 2), 6))
+
+
+def test_full_binding_chain_matches_naive(cuda):
+    # T/test_chebnd.py:588-600 pattern (batched = naive), seed 44
+    rng = np.random.default_rng(44)
+    for _ in range(10):
+        ndim = int(rng.integers(1, 5))
+        count = int(rng.integers(1, 33))
+        bases = tuple(cn.make_basis(int(rng.integers(1, 7)), -1.0, 1.0) for _ in range(ndim))
+        sc = rng.standard_normal(tuple(b.size for b in bases) + (count,))
+        pts = rng.uniform(-1.0, 1.0, (ndim, count))
+        cur = cn.TensorStack(bases, sc)
+        for d in range(ndim):
+            g = cn.make_gather_index(cur.coefficients.shape[:-1], count)
+            cur = cn.eval_diagonal_batch(cur, pts[d], g)
+        naive = np.array([orc.eval_full(sc[..., j], pts[:, j]) for j in range(count)])
+        np.testing.assert_allclose(cur.coefficients, naive, atol=1e-11)
+
+
+def test_basis_matrix_and_private_kernels(cuda):
+    pts = np.linspace(-1, 1, 9)
+    close(cn.basis_matrix(pts, 6), np.cos(np.arange(7)[None, :] * np.arccos(pts)[:, None]), rtol=0, atol=1e-13)
+    from paper_2307_04688_b200 import chebnd as nd
+
+    rng = np.random.default_rng(3)
+    B = rng.standard_normal((5, 4))
+    F = rng.standard_normal((4, 7))
+    close(nd._bind_rows(B, F), B @ F)
+    S = rng.standard_normal((3, 4, 7))
+    close(nd._bind_shared(B, S), np.matmul(B, S))
+    Bd = rng.standard_normal((3, 4))
+    close(nd._bind_diagonal(Bd, S), np.matmul(Bd[:, None, :], S)[:, 0, :])
+    close(nd._row_basis(pts, 5), orc.row_basis(pts, 5))
+
+
+def test_eval_1d_clenshaw_derivative(cuda):
+    rng = np.random.default_rng(9)
+    coef = rng.standard_normal(10)
+    c = cn.CoefVector(coef, cn.make_basis(9, -1.0, 1.0))
+    xs = np.linspace(-1, 1, 21)
+    close(cn.eval_1d(c, xs), orc.clenshaw(coef, xs))
+    assert cn.eval_1d(c, 0.7) == pytest.approx(orc.clenshaw(coef, 0.7), abs=1e-13)
+    batch = rng.standard_normal((6, 4, 3))
+    xb = rng.uniform(-1, 1, (4, 3))
+    close(cn.clenshaw(batch, xb), orc.clenshaw(batch, xb))
+    close(cn.derivative_array(batch.transpose(1, 2, 0)), orc.derivative_array(batch.transpose(1, 2, 0)))
+    with pytest.raises(ValueError):
+        cn.eval_1d(c, 1.0 + 1e-9)
+
+
+# ------------------------------------------------------------------------------------------------
+# K3 structured evaluation, K4 loop
+# ------------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("shape,k", [((13, 13, 13), (25, 7, 3)), ((5, 4, 3, 6), (2, 3, 4, 5)), ((17,), (40,)),
+                                     ((3, 3, 3, 3, 3, 3), (5, 5, 5, 5, 5, 5))])
+def test_eval_grid(cuda, shape, k):
+    rng = np.random.default_rng(sum(shape))
+    coef = rng.standard_normal(shape)
+    t = cn.CoefTensor([cn.make_basis(d - 1, -1.0, 1.0) for d in shape], coef)
+    targets = [np.linspace(-1, 1, kk) for kk in k]
+    close(cn.eval_grid(t, targets), orc.eval_grid(coef, targets))
+
+
+@pytest.mark.parametrize("J,n,steps", [(2, 9, 7), (4, 5, 4), (6, 3, 3), (3, 17, 5), (4, 17, 2)])
+def test_advect_loop(cuda, J, n, steps):
+    rng = np.random.default_rng(1000 + J * n)
+    A = rng.uniform(-0.5, 0.5, (J, J))
+    axes = workloads.grid_axes(n, J)
+    V0 = np.exp(sum(np.sin(np.pi * 1.3 * g) for g in np.meshgrid(*axes, indexing="ij")))
+    got = cn.advect_loop(V0, bases_for(J, n), A, 0.01, steps)
+    ref = orc.advect_loop(V0, A, 0.01, steps)
+    close(got, ref)
+    got_ng = cn.advect_loop(V0, bases_for(J, n), A, 0.01, steps, use_graph=False)
+    assert np.array_equal(got, got_ng)
+
+
+def test_advect_loop_config3_prefix(cuda):
+    w = workloads.make("3", steps=3)
+    got = cn.advect_loop(w.values, bases_for(w.J, w.n), w.A, w.dt, w.steps)
+    close(got, orc.advect_loop(w.values, w.A, w.dt, w.steps))
