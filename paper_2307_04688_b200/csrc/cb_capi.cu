@@ -192,7 +192,7 @@ int cb_eval_points(int J, const int64_t* n, const double* d_coef, int64_t M, con
   if (rc) return rc;
   if (M < 0) return fail(CB_EINVAL, "cb_eval_points: negative point count");
   EvalLayout L = layout_of(J, n);
-  CB_CUDA(eval_points(L, d_coef, M, d_points, nullptr, d_out, static_cast<Status*>(d_status), flags & 15,
+  CB_CUDA(eval_points(L, d_coef, M, d_points, nullptr, d_out, static_cast<Status*>(d_status), flags & 0xffff,
                       static_cast<cudaStream_t>(stream)),
           "cb_eval_points");
   return CB_OK;
