@@ -625,7 +625,10 @@ def ncu_traffic(kernel: str, cfg: str):
     try:
         with open(NCU_SUMMARY) as f:
             s = json.load(f)
-        return s.get(cfg, {}).get(kernel, {}).get("dram_bytes_per_launch")
+        ent = s.get(cfg, {}).get(kernel)
+        if isinstance(ent, list):  # multi-launch kernel sequence (e.g. the structured passes): per step
+            return sum(e.get("dram_bytes_per_launch", 0) for e in ent)
+        return (ent or {}).get("dram_bytes_per_launch")
     except (OSError, ValueError):
         return None
 

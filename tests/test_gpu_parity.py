@@ -255,7 +255,8 @@ def test_eval_1d_clenshaw_derivative(cuda):
 # ------------------------------------------------------------------------------------------------
 
 @pytest.mark.parametrize("shape,k", [((13, 13, 13), (25, 7, 3)), ((5, 4, 3, 6), (2, 3, 4, 5)), ((17,), (40,)),
-                                     ((3, 3, 3, 3, 3, 3), (5, 5, 5, 5, 5, 5))])
+                                     ((3, 3, 3, 3, 3, 3), (5, 5, 5, 5, 5, 5)), ((5, 5, 5), (4, 4, 4)),
+                                     ((13, 13, 13, 13), (25, 25, 25, 25)), ((4, 17, 17), (3, 25, 25))])
 def test_eval_grid(cuda, shape, k):
     rng = np.random.default_rng(sum(shape))
     coef = rng.standard_normal(shape)
