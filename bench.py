@@ -381,7 +381,7 @@ def run_ours(args):
         build_s = statistics.mean(build_ms) / 1000.0
         achieved_tf = flops_pt * M / eval_s / 1e12
         roofline = {
-            "bound": "fp64", "kernel": "eval_dmma_kernel (K2, DMMA.8x8x4)",
+            "bound": "fp64", "kernel": lib.cb_last_eval_plan().decode(),
             "achieved": achieved_tf, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
             "frac": achieved_tf / peaks["fp64_tflops"], "peak_source": peaks["fp64_source"],
             "algorithmic": f"{flops_pt} flop/point x {M} points per launch",
@@ -506,7 +506,7 @@ def run_ours(args):
         build_s = min(bl) / 1000.0
         achieved_tf = flops_pt * M / eval_s / 1e12
         roofline = {
-            "bound": "fp64", "kernel": "eval_dmma_kernel (K2, advected nodes)", "achieved": achieved_tf,
+            "bound": "fp64", "kernel": lib.cb_last_eval_plan().decode() + " on advected nodes", "achieved": achieved_tf,
             "peak": peaks["fp64_tflops"], "unit": "TFLOP/s", "frac": achieved_tf / peaks["fp64_tflops"],
             "peak_source": peaks["fp64_source"], "algorithmic": f"{flops_pt} flop/point x {M} nodes per launch",
             "traffic": ncu_traffic("eval_dmma_kernel", cfg),

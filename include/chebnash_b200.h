@@ -46,6 +46,10 @@ const char* cb_last_error(void);
 /* Number of kernels this library has launched in the process (graph replays not included). */
 int64_t cb_kernel_launches(void);
 
+/* Description of the evaluator kernel / plan chosen by the last cb_eval_points or
+ * cb_eval_advected call on this thread (diagnostics, bench reporting). */
+const char* cb_last_eval_plan(void);
+
 /* Device inventory: number of visible CUDA devices (0 without a GPU), SM count and compute
  * capability of the current device.  Never fails on a CPU-only host. */
 int cb_runtime_info(int* device_count, int* sm_count, int* cc_major, int* cc_minor);

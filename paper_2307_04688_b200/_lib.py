@@ -28,6 +28,7 @@ SIGNATURES = {
     "cb_abi_version": (_c_int, []),
     "cb_last_error": (ctypes.c_char_p, []),
     "cb_kernel_launches": (_c_i64, []),
+    "cb_last_eval_plan": (ctypes.c_char_p, []),
     "cb_runtime_info": (_c_int, [ctypes.POINTER(_c_int)] * 4),
     "cb_eval_layout": (_c_int, [_c_int, _i64p, _i64p]),
     "cb_pack_eval": (_c_int, [_c_int, _i64p, _vp, _vp, _vp]),

@@ -99,6 +99,8 @@ const char* cb_last_error(void) { return g_last_error.c_str(); }
 
 int64_t cb_kernel_launches(void) { return launch_count(); }
 
+const char* cb_last_eval_plan(void) { return last_eval_plan(); }
+
 int cb_runtime_info(int* device_count, int* sm_count, int* cc_major, int* cc_minor) {
   int cnt = 0;
   if (cudaGetDeviceCount(&cnt) != cudaSuccess) {

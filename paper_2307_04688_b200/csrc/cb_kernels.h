@@ -40,6 +40,7 @@ struct AdvectSpec {
   double lo[kMaxDims], hi[kMaxDims];  // state box per dim (the grid basis interval)
   int source;               // subtract dt*|x|^2 of the (unclipped) node
 };
+const char* last_eval_plan();  // kernel / plan chosen by the last eval_points on this thread
 cudaError_t eval_points(const EvalLayout& L, const double* coef, long long M, const double* points,
                         const AdvectSpec* adv, double* out, Status* st, int force_generic, cudaStream_t stream);
 

@@ -100,7 +100,9 @@ def test_eval_points_baseline_shapes(cuda, cfg, M):
 
 
 @pytest.mark.parametrize("shape", [(5,), (17,), (3, 4), (17, 17), (2, 9, 3), (6, 1, 5), (1, 1, 1), (9, 9, 9, 9),
-                                   (4, 3, 5, 2, 3), (3, 3, 3, 3, 3, 3), (2, 2, 2, 2, 2, 2, 2, 2), (33, 33, 33)])
+                                   (4, 3, 5, 2, 3), (3, 3, 3, 3, 3, 3), (2, 2, 2, 2, 2, 2, 2, 2), (33, 33, 33),
+                                   # row-contraction kernel: K % 8 tails 1, 2, 3 and padded
+                                   (17, 17, 18), (20, 15, 19), (16, 17, 12), (64, 5, 9), (120, 3, 33), (7, 6, 7, 41)])
 @pytest.mark.parametrize("generic", [False, True])
 def test_eval_points_ragged(cuda, shape, generic):
     rng = np.random.default_rng(len(shape) * 100 + sum(shape))
