@@ -307,6 +307,146 @@ cudaError_t launch_pass(PassParams& p, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+
+// ------------------------------------------------------------------------------------------
+// Fiber-parallel mode pass (one launch per transformed mode): thread = one fiber along the mode,
+// i.e. one (n)-vector of the tensor with every other index fixed.  Fibers are enumerated with the
+// innermost remaining index fastest, so a warp's loads/stores are coalesced whenever the mode is
+// not the innermost one.  Any strided layout works for input and output (dense C-order tensors,
+// the pitched eval layout, stacks with a trailing member axis), so the first pass can read the
+// dense samples and write the eval layout while later passes run in place.  The folded matrix
+// rides in the kernel parameters and unrolled FMAs take it as constant-bank operands.
+// ------------------------------------------------------------------------------------------
+constexpr int kFiberThreads = 128;
+constexpr int kFMat = 34 * 18;
+
+struct FiberParams {
+  const double* in;
+  double* out;
+  Status* st;
+  int check_finite;
+  int nother;                          // number of other (non-transformed) dims
+  int nd[kMaxDims + 1];                // their sizes, enumeration order (last = fastest)
+  FastDiv fd[kMaxDims + 1];
+  long long sin[kMaxDims + 1], sout[kMaxDims + 1];  // their strides (elements)
+  long long kin, kout;                 // stride of the transformed mode
+  long long fibers;
+  double M[kFMat];                     // folded matrix, row pitch n/2 + 1 (n <= 34)
+};
+
+template <int TN>
+__global__ void __launch_bounds__(kFiberThreads) fiber_pass_kernel(const __grid_constant__ FiberParams p) {
+  const long long f = static_cast<long long>(blockIdx.x) * kFiberThreads + threadIdx.x;
+  if (f >= p.fibers) return;
+  long long oin = 0, oout = 0;
+  uint32_t rem = static_cast<uint32_t>(f);
+#pragma unroll
+  for (int i = kMaxDims; i >= 0; --i) {
+    if (i < p.nother) {
+      uint32_t q, r;
+      p.fd[i].divmod(rem, q, r);
+      oin += static_cast<long long>(r) * p.sin[i];
+      oout += static_cast<long long>(r) * p.sout[i];
+      rem = q;
+    }
+  }
+  const double* src = p.in + oin;
+  double* dst = p.out + oout;
+  if constexpr (TN == 1) {
+    dst[0] = src[0];
+    if (p.check_finite && !isfinite(src[0])) atomicAdd(&p.st->nonfinite, 1u);
+  } else {
+    constexpr int N = TN - 1, H = TN / 2, P = H + 1;
+    double v[TN];
+#pragma unroll
+    for (int k = 0; k < TN; ++k) v[k] = src[k * p.kin];
+    if (p.check_finite) {
+      bool ok = true;
+#pragma unroll
+      for (int k = 0; k < TN; ++k) ok &= isfinite(v[k]);
+      if (!ok) atomicAdd(&p.st->nonfinite, 1u);
+    }
+    double e[H], o[H];
+#pragma unroll
+    for (int k = 0; k < H; ++k) {
+      e[k] = v[k] + v[N - k];
+      o[k] = v[k] - v[N - k];
+    }
+#pragma unroll
+    for (int l = 0; l <= N; ++l) {
+      double acc = 0.0;
+      if ((l & 1) == 0) {
+#pragma unroll
+        for (int k = 0; k < H; ++k) acc = fma(p.M[l * P + k], e[k], acc);
+        if constexpr (TN & 1) acc = fma(p.M[l * P + H], v[H], acc);
+      } else {
+#pragma unroll
+        for (int k = 0; k < H; ++k) acc = fma(p.M[l * P + k], o[k], acc);
+      }
+      dst[l * p.kout] = acc;
+    }
+  }
+}
+
+template <int TN>
+struct FTag { static constexpr int value = TN; };
+
+template <typename F>
+bool dispatch_fiber(int n, F&& f) {
+  switch (n) {
+#define CB_CASE(v) case v: f(FTag<v>{}); return true;
+    CB_CASE(1) CB_CASE(2) CB_CASE(3) CB_CASE(4) CB_CASE(5) CB_CASE(6) CB_CASE(7) CB_CASE(8)
+    CB_CASE(9) CB_CASE(10) CB_CASE(11) CB_CASE(12) CB_CASE(13) CB_CASE(14) CB_CASE(15) CB_CASE(16)
+    CB_CASE(17) CB_CASE(18) CB_CASE(19) CB_CASE(20) CB_CASE(21) CB_CASE(22) CB_CASE(23) CB_CASE(24)
+    CB_CASE(25) CB_CASE(26) CB_CASE(27) CB_CASE(28) CB_CASE(29) CB_CASE(30) CB_CASE(31) CB_CASE(32)
+    CB_CASE(33) CB_CASE(34)
+#undef CB_CASE
+    default: return false;
+  }
+}
+
+// One mode pass over a strided tensor: dims (sizes) with input strides `sin` and output strides
+// `sout`; mode `d` is transformed.  Returns false when n is outside the unrolled range.
+bool launch_fiber_pass(int nd, const long long* sizes, const long long* sin, const long long* sout, int d,
+                       const double* in, double* out, Status* st, int check_finite, cudaStream_t stream,
+                       cudaError_t* err) {
+  FiberParams p{};
+  p.in = in;
+  p.out = out;
+  p.st = st;
+  p.check_finite = check_finite;
+  long long fibers = 1;
+  int j = 0;
+  for (int i = 0; i < nd; ++i) {
+    if (i == d) continue;
+    p.nd[j] = static_cast<int>(sizes[i]);
+    p.fd[j] = FastDiv(static_cast<uint32_t>(sizes[i]));
+    p.sin[j] = sin[i];
+    p.sout[j] = sout[i];
+    fibers *= sizes[i];
+    ++j;
+  }
+  p.nother = j;
+  p.kin = sin[d];
+  p.kout = sout[d];
+  p.fibers = fibers;
+  const int n = static_cast<int>(sizes[d]);
+  const int N = n - 1, P = n / 2 + 1;
+  if (n > 34) return false;
+  for (int l = 0; l < n; ++l)
+    for (int c = 0; c < P; ++c) p.M[l * P + c] = (c <= N) ? transform_entry(l, c, N) : 0.0;
+  const long long grid = (fibers + kFiberThreads - 1) / kFiberThreads;
+  *err = cudaSuccess;
+  if (grid <= 0) return true;
+  dispatch_fiber(n, [&](auto tag) {
+    constexpr int TN = decltype(tag)::value;
+    fiber_pass_kernel<TN><<<static_cast<unsigned>(grid), kFiberThreads, 0, stream>>>(p);
+  });
+  count_launch();
+  *err = cudaGetLastError();
+  return true;
+}
+
 }  // namespace
 
 // Transform the consecutive axes [a0, a1) of a dense C-order array `shape` (ndim dims).
@@ -323,6 +463,60 @@ cudaError_t transform_axes(int ndim, const long long* shape, int a0, int a1, con
   }
   for (int d = a0; d < a1; ++d)
     if (shape[d] < 1 || shape[d] > kMaxGenericN) return cudaErrorInvalidValue;
+  {
+    long long total = 1;
+    bool small_modes = true;
+    long long min_fibers = -1;
+    for (int d = 0; d < ndim; ++d) total *= shape[d];
+    for (int d = a0; d < a1; ++d) {
+      if (shape[d] > 34) small_modes = false;
+      const long long fb = total / shape[d];
+      if (min_fibers < 0 || fb < min_fibers) min_fibers = fb;
+    }
+    if (small_modes && min_fibers >= 2048 && ndim <= kMaxDims + 1) {
+      // strides: input dense C-order; output dense or the eval layout (leading rows x Kp pitch)
+      long long sin[kMaxDims + 1], sout[kMaxDims + 1];
+      long long acc = 1;
+      for (int d = ndim - 1; d >= 0; --d) {
+        sin[d] = acc;
+        acc *= shape[d];
+      }
+      if (evl) {
+        long long a2 = 1;
+        for (int d = ndim - 1; d >= ndim - evl->q; --d) {
+          sout[d] = a2;
+          a2 *= shape[d];
+        }
+        long long a3 = evl->Kp;
+        for (int d = ndim - evl->q - 1; d >= 0; --d) {
+          sout[d] = a3;
+          a3 *= shape[d];
+        }
+        // zero the pad columns / rows (never written by the passes)
+        if (evl->Kp > evl->K) {
+          cudaError_t e = cudaMemset2DAsync(out + evl->K, sizeof(double) * evl->Kp, 0, sizeof(double) * (evl->Kp - evl->K),
+                                            evl->R, stream);
+          if (e != cudaSuccess) return e;
+        }
+      } else {
+        for (int d = 0; d < ndim; ++d) sout[d] = sin[d];
+      }
+      const double* cur = in;
+      bool first = true;
+      for (int d = a1 - 1; d >= a0; --d) {
+        cudaError_t err = cudaSuccess;
+        if (!launch_fiber_pass(ndim, shape, first ? sin : sout, sout, d, cur, out, st, first ? check_finite : 0,
+                               stream, &err))
+          return cudaErrorInvalidValue;
+        if (err != cudaSuccess) return err;
+        cur = out;
+        first = false;
+      }
+      if (evl && evl->R8 > evl->R)
+        return cudaMemsetAsync(out + evl->R * evl->Kp, 0, sizeof(double) * (evl->R8 - evl->R) * evl->Kp, stream);
+      return cudaSuccess;
+    }
+  }
   long long inner = 1;
   for (int d = a1; d < ndim; ++d) inner *= shape[d];
   long long outer = 1;
