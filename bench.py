@@ -385,7 +385,7 @@ def run_ours(args):
             "achieved": achieved_tf, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
             "frac": achieved_tf / peaks["fp64_tflops"], "peak_source": peaks["fp64_source"],
             "algorithmic": f"{flops_pt} flop/point x {M} points per launch",
-            "traffic": ncu_traffic("eval_dmma_kernel", cfg),
+            "traffic": ncu_traffic(lib.cb_last_eval_plan().decode().split("<")[0], cfg),
         }
         build_bytes = 16 * n ** J
         roofline_build = {
