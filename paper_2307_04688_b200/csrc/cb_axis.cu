@@ -218,6 +218,143 @@ __global__ void derivative_kernel(long long rows, int L, const double* in, doubl
   }
 }
 
+
+// K3 fused final pair of structured modes:  in (n, n, R') -> out (R', k, k)
+//   out[r'][ia][ib] = sum_{la, lb} Ea[ia][la] Eb[ib][lb] in[la][lb][r'].
+// A CTA owns RT consecutive r'.  Step 1 contracts lb (Z[la][r'][ib]), step 2 contracts la and
+// writes the (RT x k x k) output tile with lanes along ib (contiguous in memory).  The evaluation
+// matrices ride in the kernel parameters (constant bank): every FMA takes them as a direct
+// operand, each thread keeps its n inputs in registers and produces k outputs (k independent
+// FMA chains).  Saves the write + re-read of the largest intermediate (13 x 25^5 for config 5a).
+template <int N, int K>
+struct Fused2Params {
+  double Ea[K * N];
+  double Eb[K * N];
+  const double* in;
+  double* out;
+  long long R;
+};
+
+constexpr int kF2RT = 16;      // r' per tile
+constexpr int kF2Warps = 7;    // 7 x 32 = 224 >= 13 * 16 step-1 rows; 3 CTAs / SM
+constexpr int kF2Threads = kF2Warps * 32;
+constexpr int kF2IB = 5;       // K <= 25 (5 blocks)       // outputs per thread item (compile-time constant-bank indices)
+
+// step 1, output block B: z[ib] for ib in [B*5, B*5+5) from the N inputs v (row la, column rt)
+template <int N, int K, int B>
+__device__ __forceinline__ void f2_step1(const Fused2Params<N, K>& p, const double* v, double* z) {
+#pragma unroll
+  for (int j = 0; j < kF2IB; ++j) {
+    const int ib = B * kF2IB + j;
+    if (ib < K) {
+      double acc = 0.0;
+#pragma unroll
+      for (int lb = 0; lb < N; ++lb) acc = fma(p.Eb[ib * N + lb], v[lb], acc);
+      z[ib] = acc;
+    }
+  }
+}
+
+template <int N, int K, int B>
+__device__ __forceinline__ void f2_step2(const Fused2Params<N, K>& p, const double* v, double* dst) {
+#pragma unroll
+  for (int j = 0; j < kF2IB; ++j) {
+    const int ia = B * kF2IB + j;
+    if (ia < K) {
+      double acc = 0.0;
+#pragma unroll
+      for (int la = 0; la < N; ++la) acc = fma(p.Ea[ia * N + la], v[la], acc);
+      dst[ia * K] = acc;
+    }
+  }
+}
+
+template <int N, int K>
+__global__ void __launch_bounds__(kF2Threads, 3) fused2_kernel(const __grid_constant__ Fused2Params<N, K> p) {
+  extern __shared__ __align__(16) double f2sm[];
+  double* sX = f2sm;                   // [N*N][RT]
+  double* sZ = f2sm + N * N * kF2RT;   // [N][RT][K]
+  constexpr int NB = (K + kF2IB - 1) / kF2IB;
+  constexpr int C1 = (N * kF2RT + 31) / 32;   // 32-row chunks of step 1 (per output block)
+  constexpr int C2 = (K * kF2RT + 31) / 32;   // 32-item chunks of step 2 (per output block)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // one tile per CTA (no persistent loop: keeps the constant-bank operands from being hoisted
+  // into registers across iterations)
+  {
+    const long long r0 = static_cast<long long>(blockIdx.x) * kF2RT;
+    const int rt_n = static_cast<int>(min(static_cast<long long>(kF2RT), p.R - r0));
+    for (int e = threadIdx.x; e < N * N * kF2RT; e += blockDim.x) {
+      const int row = e / kF2RT, rt = e % kF2RT;
+      sX[e] = (rt < rt_n) ? __ldg(p.in + static_cast<long long>(row) * p.R + r0 + rt) : 0.0;
+    }
+    __syncthreads();
+    // step 1: Z[la][rt][ib] = sum_lb Eb[ib][lb] X[la][lb][rt]; task = (block, chunk), warp-uniform block
+#pragma unroll
+    for (int it = 0; it < (NB * C1 + kF2Warps - 1) / kF2Warps; ++it) {
+      const int task = warp + it * kF2Warps;
+      if (task >= NB * C1) break;
+      const int blk = task / C1, w = (task % C1) * 32 + lane;
+      if (w < N * kF2RT) {
+        const int la = w / kF2RT, rt = w % kF2RT;
+        double v[N];
+#pragma unroll
+        for (int lb = 0; lb < N; ++lb) v[lb] = sX[(la * N + lb) * kF2RT + rt];
+        double* z = sZ + (la * kF2RT + rt) * K;
+        switch (blk) {
+          case 0: f2_step1<N, K, 0>(p, v, z); break;
+          case 1: if constexpr (NB > 1) f2_step1<N, K, 1>(p, v, z); break;
+          case 2: if constexpr (NB > 2) f2_step1<N, K, 2>(p, v, z); break;
+          case 3: if constexpr (NB > 3) f2_step1<N, K, 3>(p, v, z); break;
+          default: if constexpr (NB > 4) f2_step1<N, K, 4>(p, v, z); break;
+        }
+      }
+    }
+    __syncthreads();
+    // step 2: out[r0+rt][ia][ib] = sum_la Ea[ia][la] Z[la][rt][ib]; lanes along ib (contiguous)
+#pragma unroll
+    for (int it = 0; it < (NB * C2 + kF2Warps - 1) / kF2Warps; ++it) {
+      const int task = warp + it * kF2Warps;
+      if (task >= NB * C2) break;
+      const int blk = task / C2, w = (task % C2) * 32 + lane;
+      const int rt = w / K, ib = w % K;
+      if (w < K * kF2RT && rt < rt_n) {
+        double v[N];
+#pragma unroll
+        for (int la = 0; la < N; ++la) v[la] = sZ[(la * kF2RT + rt) * K + ib];
+        double* dst = p.out + (r0 + rt) * (K * K) + ib;
+        switch (blk) {
+          case 0: f2_step2<N, K, 0>(p, v, dst); break;
+          case 1: if constexpr (NB > 1) f2_step2<N, K, 1>(p, v, dst); break;
+          case 2: if constexpr (NB > 2) f2_step2<N, K, 2>(p, v, dst); break;
+          case 3: if constexpr (NB > 3) f2_step2<N, K, 3>(p, v, dst); break;
+          default: if constexpr (NB > 4) f2_step2<N, K, 4>(p, v, dst); break;
+        }
+      }
+    }
+  }
+}
+
+template <int N, int K>
+cudaError_t launch_fused2(const double* Ea_dev, const double* Eb_dev, const double* in, double* out, long long R,
+                          cudaStream_t stream) {
+  Fused2Params<N, K> p;
+  // the evaluation matrices become kernel parameters (constant bank): fetch them (tiny, sync)
+  cudaError_t e = cudaMemcpyAsync(p.Ea, Ea_dev, sizeof(double) * K * N, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(p.Eb, Eb_dev, sizeof(double) * K * N, cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return e;
+  p.in = in;
+  p.out = out;
+  p.R = R;
+  const long long g = (R + kF2RT - 1) / kF2RT;
+  if (g > 0x7fffffffLL) return cudaErrorInvalidValue;
+  const size_t smem = sizeof(double) * (N * N + N * K) * kF2RT;
+  ensure_smem_attr(reinterpret_cast<const void*>(fused2_kernel<N, K>), 200 * 1024);
+  fused2_kernel<N, K><<<static_cast<unsigned>(g), kF2Threads, smem, stream>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
 unsigned grid_for(long long total, int threads) {
   long long g = (total + threads - 1) / threads;
   const long long cap = static_cast<long long>(num_sms()) * 32;
@@ -313,9 +450,18 @@ cudaError_t gather_take_f(int ndim_in, const long long* shape_in, const double* 
   return cudaGetLastError();
 }
 
+// the last two modes fused when their sizes have an instantiated kernel (launch_fused2)
+static bool grid_fuse_last_two(const EvalLayout& L, const long long* k) {
+  const int J = L.J;
+  if (J < 3 || L.n[J - 2] != L.n[J - 1] || k[J - 2] != k[J - 1]) return false;
+  const long long n = L.n[J - 1], kk = k[J - 1];
+  return (n == 13 && kk == 25) || (n == 5 && kk == 4);
+}
+
 long long eval_grid_work_elems(const EvalLayout& L, const long long* k) {
   long long dense = 1;
   for (int d = 0; d < L.J; ++d) dense *= L.n[d];
+  dense = dense / L.K * L.Kp;  // the passes may carry the K padding (q = 2 fused path)
   long long mx = dense;
   long long cur = dense;
   for (int d = 0; d + 1 < L.J; ++d) {
@@ -335,14 +481,20 @@ cudaError_t eval_grid(const EvalLayout& L, const double* coef, const long long* 
   double* bufA = work;
   double* bufB = work + need / 2;
   const double* cur = coef;
-  if (L.Kp != L.K) {
+  const bool fuse = grid_fuse_last_two(L, k);
+  long long total = dense;
+  if (fuse && L.q == 2) {
+    // the eval layout's trailing K = n_{J-2} * n_{J-1} (padded to Kp) is exactly the fused pair:
+    // the single passes carry the padded rows along and the fused kernel ignores rows >= n^2
+    total = dense / L.K * L.Kp;
+  } else if (L.Kp != L.K) {
     cudaError_t err = cudaMemcpy2DAsync(bufA, sizeof(double) * L.K, coef, sizeof(double) * L.Kp,
                                         sizeof(double) * L.K, L.R, cudaMemcpyDeviceToDevice, stream);
     if (err != cudaSuccess) return err;
     cur = bufA;
   }
-  long long total = dense;
-  for (int d = 0; d < J; ++d) {
+  const int single_passes = fuse ? J - 2 : J;
+  for (int d = 0; d < single_passes; ++d) {
     const long long R = total / L.n[d];
     double* dst = (d == J - 1) ? out : ((cur == bufA) ? bufB : bufA);
     cudaError_t err = contract_axis(1, static_cast<int>(L.n[d]), R, 1, static_cast<int>(k[d]), E[d], cur, dst, 0, 1,
@@ -350,6 +502,12 @@ cudaError_t eval_grid(const EvalLayout& L, const double* coef, const long long* 
     if (err != cudaSuccess) return err;
     total = R * k[d];
     cur = dst;
+  }
+  if (fuse) {
+    const long long n = L.n[J - 1], kk = k[J - 1];
+    const long long R = total / ((L.q == 2) ? L.Kp : n * n);
+    if (n == 13 && kk == 25) return launch_fused2<13, 25>(E[J - 2], E[J - 1], cur, out, R, stream);
+    if (n == 5 && kk == 4) return launch_fused2<5, 4>(E[J - 2], E[J - 1], cur, out, R, stream);
   }
   return cudaSuccess;
 }

@@ -258,7 +258,10 @@ def test_eval_1d_clenshaw_derivative(cuda):
 
 @pytest.mark.parametrize("shape,k", [((13, 13, 13), (25, 7, 3)), ((5, 4, 3, 6), (2, 3, 4, 5)), ((17,), (40,)),
                                      ((3, 3, 3, 3, 3, 3), (5, 5, 5, 5, 5, 5)), ((5, 5, 5), (4, 4, 4)),
-                                     ((13, 13, 13, 13), (25, 25, 25, 25)), ((4, 17, 17), (3, 25, 25))])
+                                     ((13, 13, 13, 13), (25, 25, 25, 25)), ((4, 17, 17), (3, 25, 25)),
+                                     # fused last pair: q = 1 (unpadded copy) and q = 2 (padded rows carried)
+                                     ((3, 5, 5), (2, 4, 4)), ((2, 13, 13), (3, 25, 25)), ((7, 3, 13, 13), (5, 4, 25, 25)),
+                                     ((40, 5, 5), (9, 4, 4))])
 def test_eval_grid(cuda, shape, k):
     rng = np.random.default_rng(sum(shape))
     coef = rng.standard_normal(shape)
