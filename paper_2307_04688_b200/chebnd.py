@@ -233,9 +233,9 @@ def _unpack(shape, eval_dev):
 # basis rows and the private contraction kernels the solver imports (S/solver.py:37-48)
 # ---------------------------------------------------------------------------------------------
 
-def _basis_device(points_dev, size: int, clamp: bool, status=None):
+def _basis_device(points_dev, size: int, clamp: bool, status=None, out=None):
     k = int(points_dev.numel())
-    out = _lib.empty((k, size))
+    out = _lib.empty((k, size)) if out is None else out
     _lib.check(
         _lib.load().cb_basis_matrix(k, _lib.ptr(points_dev), int(size), _lib.ptr(out), _lib.ptr(status),
                                     1 if clamp else 0, _lib.stream_handle()),
@@ -504,14 +504,21 @@ def eval_grid(tensor: CoefTensor, targets):
     if len(targets) != J:
         raise ValueError(f"need {J} target lists, got {len(targets)}")
     shape = tensor.shape
-    Es, ks = [], []
-    st = _lib.new_status()
-    for j, t in enumerate(targets):
+    tvs = []
+    for t in targets:
         tv = t if _is_tensor(t) else np.asarray(t, dtype=float)
         if tv.ndim != 1 or tv.shape[0] == 0:
             raise ValueError("points must be a non-empty one-dimensional list")
-        Es.append(_basis_device(_lib.to_device(tv), shape[j], True, st))
-        ks.append(int(tv.shape[0]))
+        tvs.append(tv)
+    ks = [int(tv.shape[0]) for tv in tvs]
+    # all J evaluation matrices in one allocation (the C side fetches them with one copy)
+    Eall = _lib.empty((sum(k * n for k, n in zip(ks, shape)),))
+    Es, off = [], 0
+    st = _lib.new_status()
+    for j, tv in enumerate(tvs):
+        view = Eall[off:off + ks[j] * shape[j]].view(ks[j], shape[j])
+        Es.append(_basis_device(_lib.to_device(tv), shape[j], True, st, out=view))
+        off += ks[j] * shape[j]
     lib = _lib.load()
     work_elems = int(lib.cb_eval_grid_workspace(J, _lib.i64_array(shape), _lib.i64_array(ks)))
     work = _lib.empty((max(1, work_elems),))

@@ -10,6 +10,9 @@
 //   eval_grid         : J successive rotating mode products with k_j x n_j evaluation matrices
 //                       (the paper's pagemtimes evaluation P:385-417; BASELINE config 5a).
 //   basis_matrix, gather_index, gather_take_f : S/chebnd.py:114-132, 243-272, 97-111.
+#include <mutex>
+#include <vector>
+
 #include "cb_common.cuh"
 #include "cb_kernels.h"
 
@@ -226,10 +229,15 @@ __global__ void derivative_kernel(long long rows, int L, const double* in, doubl
 // matrices ride in the kernel parameters (constant bank): every FMA takes them as a direct
 // operand, each thread keeps its n inputs in registers and produces k outputs (k independent
 // FMA chains).  Saves the write + re-read of the largest intermediate (13 x 25^5 for config 5a).
+// Evaluation matrices of the structured passes live in two constant-memory slots, filled by a
+// stream-ordered device-to-device copy right before the kernel that reads them (no host sync);
+// every DFMA then takes its matrix entry as a constant-bank operand.  Calls on different streams
+// are ordered through ConstSlotGuard (eval_grid).
+constexpr int kCESlot = 1024;
+__constant__ double cGridE[2][kCESlot];
+
 template <int N, int K>
 struct Fused2Params {
-  double Ea[K * N];
-  double Eb[K * N];
   const double* in;
   double* out;
   long long R;
@@ -249,7 +257,7 @@ __device__ __forceinline__ void f2_step1(const Fused2Params<N, K>& p, const doub
     if (ib < K) {
       double acc = 0.0;
 #pragma unroll
-      for (int lb = 0; lb < N; ++lb) acc = fma(p.Eb[ib * N + lb], v[lb], acc);
+      for (int lb = 0; lb < N; ++lb) acc = fma(cGridE[1][ib * N + lb], v[lb], acc);
       z[ib] = acc;
     }
   }
@@ -263,7 +271,7 @@ __device__ __forceinline__ void f2_step2(const Fused2Params<N, K>& p, const doub
     if (ia < K) {
       double acc = 0.0;
 #pragma unroll
-      for (int la = 0; la < N; ++la) acc = fma(p.Ea[ia * N + la], v[la], acc);
+      for (int la = 0; la < N; ++la) acc = fma(cGridE[0][ia * N + la], v[la], acc);
       dst[ia * K] = acc;
     }
   }
@@ -335,14 +343,15 @@ __global__ void __launch_bounds__(kF2Threads, 3) fused2_kernel(const __grid_cons
 }
 
 template <int N, int K>
-cudaError_t launch_fused2(const double* Ea_dev, const double* Eb_dev, const double* in, double* out, long long R,
+cudaError_t launch_fused2(const double* Ea, const double* Eb, const double* in, double* out, long long R,
                           cudaStream_t stream) {
-  Fused2Params<N, K> p;
-  // the evaluation matrices become kernel parameters (constant bank): fetch them (tiny, sync)
-  cudaError_t e = cudaMemcpyAsync(p.Ea, Ea_dev, sizeof(double) * K * N, cudaMemcpyDeviceToHost, stream);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(p.Eb, Eb_dev, sizeof(double) * K * N, cudaMemcpyDeviceToHost, stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  static_assert(K * N <= kCESlot, "constant slot too small");
+  cudaError_t e = cudaMemcpyToSymbolAsync(cGridE, Ea, sizeof(double) * K * N, 0, cudaMemcpyDeviceToDevice, stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyToSymbolAsync(cGridE, Eb, sizeof(double) * K * N, sizeof(double) * kCESlot,
+                                cudaMemcpyDeviceToDevice, stream);
   if (e != cudaSuccess) return e;
+  Fused2Params<N, K> p;
   p.in = in;
   p.out = out;
   p.R = R;
@@ -351,6 +360,63 @@ cudaError_t launch_fused2(const double* Ea_dev, const double* Eb_dev, const doub
   const size_t smem = sizeof(double) * (N * N + N * K) * kF2RT;
   ensure_smem_attr(reinterpret_cast<const void*>(fused2_kernel<N, K>), 200 * 1024);
   fused2_kernel<N, K><<<static_cast<unsigned>(g), kF2Threads, smem, stream>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
+
+// Rotating single-mode pass with the (K x N) evaluation matrix in the kernel parameters:
+//   out[r][j] = sum_l E[j][l] in[l][r].  One row per thread, one 256-row tile per CTA (no
+//   persistent loop, so the constant operands stay in the bank), output staged in shared memory
+//   and written as one contiguous block.
+template <int N, int K>
+struct RotParams {
+  const double* in;
+  double* out;
+  long long R;
+};
+
+constexpr int kRCThreads = 256;
+
+template <int N, int K>
+__global__ void __launch_bounds__(kRCThreads) rotate_const(const __grid_constant__ RotParams<N, K> p) {
+  extern __shared__ __align__(16) double rcs[];   // [256][K]
+  const long long r0 = static_cast<long long>(blockIdx.x) * kRCThreads;
+  const int rows = static_cast<int>(min(static_cast<long long>(kRCThreads), p.R - r0));
+  const int r = threadIdx.x;
+  if (r < rows) {
+    double v[N];
+#pragma unroll
+    for (int l = 0; l < N; ++l) v[l] = __ldg(p.in + static_cast<long long>(l) * p.R + r0 + r);
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      double acc = 0.0;
+#pragma unroll
+      for (int l = 0; l < N; ++l) acc = fma(cGridE[0][j * N + l], v[l], acc);
+      rcs[r * K + j] = acc;
+    }
+  }
+  __syncthreads();
+  double* dst = p.out + r0 * K;
+  const int cnt = rows * K;
+  for (int e = threadIdx.x; e < cnt; e += blockDim.x) dst[e] = rcs[e];
+}
+
+template <int N, int K>
+cudaError_t launch_rotate_const(const double* E, const double* in, double* out, long long R,
+                                cudaStream_t stream) {
+  static_assert(K * N <= kCESlot, "constant slot too small");
+  cudaError_t e = cudaMemcpyToSymbolAsync(cGridE, E, sizeof(double) * K * N, 0, cudaMemcpyDeviceToDevice, stream);
+  if (e != cudaSuccess) return e;
+  RotParams<N, K> p;
+  p.in = in;
+  p.out = out;
+  p.R = R;
+  const long long g = (R + kRCThreads - 1) / kRCThreads;
+  if (g > 0x7fffffffLL) return cudaErrorInvalidValue;
+  const size_t smem = sizeof(double) * kRCThreads * K;
+  ensure_smem_attr(reinterpret_cast<const void*>(rotate_const<N, K>), 200 * 1024);
+  rotate_const<N, K><<<static_cast<unsigned>(g), kRCThreads, smem, stream>>>(p);
   count_launch();
   return cudaGetLastError();
 }
@@ -450,6 +516,40 @@ cudaError_t gather_take_f(int ndim_in, const long long* shape_in, const double* 
   return cudaGetLastError();
 }
 
+
+// Orders uses of the constant slots (cGridE) across streams: a call waits for the previous call's
+// last reader (per device) before its first slot copy and records itself on exit.  Skipped while
+// the stream is being captured into a graph (the graph's own order applies).
+struct ConstSlotGuard {
+  static std::mutex& mu() {
+    static std::mutex m;
+    return m;
+  }
+  static cudaEvent_t& last(int dev) {
+    static cudaEvent_t ev[64] = {};
+    return ev[dev & 63];
+  }
+  std::lock_guard<std::mutex> lock;
+  cudaStream_t stream;
+  int dev = 0;
+  bool active = false;
+  cudaError_t err = cudaSuccess;
+  explicit ConstSlotGuard(cudaStream_t s) : lock(mu()), stream(s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    err = cudaStreamIsCapturing(stream, &cs);
+    if (err != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+    err = cudaGetDevice(&dev);
+    if (err != cudaSuccess) return;
+    cudaEvent_t& ev = last(dev);
+    if (!ev) err = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (err == cudaSuccess) err = cudaStreamWaitEvent(stream, ev, 0);
+    active = err == cudaSuccess;
+  }
+  ~ConstSlotGuard() {
+    if (active) cudaEventRecord(last(dev), stream);
+  }
+};
+
 // the last two modes fused when their sizes have an instantiated kernel (launch_fused2)
 static bool grid_fuse_last_two(const EvalLayout& L, const long long* k) {
   const int J = L.J;
@@ -494,11 +594,15 @@ cudaError_t eval_grid(const EvalLayout& L, const double* coef, const long long* 
     cur = bufA;
   }
   const int single_passes = fuse ? J - 2 : J;
+  auto const_ok = [&](int d) { return L.n[d] == 13 && k[d] == 25; };
+  ConstSlotGuard guard(stream);
+  if (guard.err != cudaSuccess) return guard.err;
   for (int d = 0; d < single_passes; ++d) {
     const long long R = total / L.n[d];
     double* dst = (d == J - 1) ? out : ((cur == bufA) ? bufB : bufA);
-    cudaError_t err = contract_axis(1, static_cast<int>(L.n[d]), R, 1, static_cast<int>(k[d]), E[d], cur, dst, 0, 1,
-                                    k[d], stream);
+    cudaError_t err = const_ok(d) ? launch_rotate_const<13, 25>(E[d], cur, dst, R, stream)
+                                  : contract_axis(1, static_cast<int>(L.n[d]), R, 1, static_cast<int>(k[d]), E[d], cur,
+                                                  dst, 0, 1, k[d], stream);
     if (err != cudaSuccess) return err;
     total = R * k[d];
     cur = dst;
