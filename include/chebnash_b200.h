@@ -86,6 +86,16 @@ int cb_transform_axes(int ndim, const int64_t* shape, int a0, int a1, const doub
 int cb_eval_points(int J, const int64_t* n, const double* d_coef, int64_t M, const double* d_points, double* d_out,
                    void* d_status, int flags, void* stream);
 
+/* K2 from host buffers — the same evaluation with (M, J) points and (M,) results in HOST memory
+ * (pinned for overlap): the points are copied up, evaluated and copied back in chunks on two
+ * internal copy streams so the PCIe transfers overlap the evaluator (solver.py:388-397 as called
+ * from host code).  d_points_ws (M*J doubles) and d_out_ws (M doubles) are device work buffers.
+ * Asynchronous with respect to the host: results are in h_out once `stream` has completed.
+ * Bitwise identical to cb_eval_points on the same inputs. */
+int cb_eval_points_host(int J, const int64_t* n, const double* d_coef, int64_t M, const double* h_points,
+                        double* h_out, double* d_points_ws, double* d_out_ws, void* d_status, int flags,
+                        void* stream);
+
 /* K4 building block — evaluate at advected grid nodes (solver.py:383-397 with a fixed linear
  * drift): for flat C-order node indices i in [node_begin, node_begin+count):
  *   x = grid node i on the box [lo, hi]^J (make_basis nodes), y = clip(x + dt*A x, lo, hi),

@@ -403,9 +403,32 @@ def eval_points(tensor: CoefTensor, points, check: bool = True):
     p = points if is_t else np.asarray(points, dtype=float)
     if p.ndim != 2 or p.shape[1] != tensor.ndim:
         raise ValueError(f"expected points of shape (M, {tensor.ndim}), got {tuple(p.shape)}")
+    if is_t and not p.is_cuda and p.is_pinned() and p.dtype == _lib.torch().float64 and p.is_contiguous():
+        return _eval_points_pinned(tensor, p, check)
     dp = _lib.to_device(p)
     out = _eval_points_device(tensor.shape, tensor.device_coefficients, dp, check=check)
     return _lib.like_input(out, points)
+
+
+def _eval_points_pinned(tensor: CoefTensor, points, check: bool):
+    """Pinned host points -> pinned host values: the C-ABI host pipeline (cb_eval_points_host)
+    overlaps the chunked H2D / evaluation / D2H."""
+    t = _lib.torch()
+    M = int(points.shape[0])
+    host_out = t.empty((M,), dtype=t.float64, pin_memory=True)
+    if M == 0:
+        return host_out
+    ws_pts = _lib.empty((M, tensor.ndim))
+    ws_out = _lib.empty((M,))
+    st = _lib.new_status() if check else None
+    _lib.check(_lib.load().cb_eval_points_host(tensor.ndim, _lib.i64_array(tensor.shape),
+                                               _lib.ptr(tensor.device_coefficients), M, points.data_ptr(),
+                                               host_out.data_ptr(), _lib.ptr(ws_pts), _lib.ptr(ws_out), _lib.ptr(st),
+                                               0, _lib.stream_handle()), "eval_points")
+    t.cuda.current_stream().synchronize()
+    if check:
+        _lib.raise_for_points(st)
+    return host_out
 
 
 def eval_full(tensor: CoefTensor, point) -> float:

@@ -200,6 +200,80 @@ int cb_eval_points(int J, const int64_t* n, const double* d_coef, int64_t M, con
   return CB_OK;
 }
 
+// Copy streams + events for the host-buffer pipeline (one set per device, created on first use).
+namespace {
+constexpr int kPipeMaxChunks = 8;
+struct Pipe {
+  cudaStream_t up = nullptr, down = nullptr;
+  cudaEvent_t start = nullptr, done = nullptr;
+  cudaEvent_t landed[kPipeMaxChunks] = {}, evaluated[kPipeMaxChunks] = {};
+};
+Pipe g_pipe[kMaxDevices];
+std::mutex g_pipe_mutex;
+
+cudaError_t pipe_for_device(Pipe** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  Pipe& p = g_pipe[dev];
+  if (!p.up) {
+    e = cudaStreamCreateWithFlags(&p.up, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p.down, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.start, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.done, cudaEventDisableTiming);
+    for (int i = 0; i < kPipeMaxChunks && e == cudaSuccess; ++i) {
+      e = cudaEventCreateWithFlags(&p.landed[i], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.evaluated[i], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) return e;
+  }
+  *out = &p;
+  return cudaSuccess;
+}
+}  // namespace
+
+int cb_eval_points_host(int J, const int64_t* n, const double* d_coef, int64_t M, const double* h_points,
+                        double* h_out, double* d_points_ws, double* d_out_ws, void* d_status, int flags,
+                        void* stream) {
+  int rc = check_dims(J, n, "cb_eval_points_host");
+  if (rc) return rc;
+  if (M < 0) return fail(CB_EINVAL, "cb_eval_points_host: negative point count");
+  if (M == 0) return CB_OK;
+  EvalLayout L = layout_of(J, n);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::lock_guard<std::mutex> lock(g_pipe_mutex);
+  Pipe* p = nullptr;
+  CB_CUDA(pipe_for_device(&p), "cb_eval_points_host");
+  // chunks of >= 2^18 points (one evaluator launch stays several waves deep), at most 8
+  long long nch = M / (1LL << 18);
+  if (nch < 1) nch = 1;
+  if (nch > kPipeMaxChunks) nch = kPipeMaxChunks;
+  const long long per = (M + nch - 1) / nch;
+  CB_CUDA(cudaEventRecord(p->start, s), "cb_eval_points_host");  // inputs (coefficients) ready
+  CB_CUDA(cudaStreamWaitEvent(p->up, p->start, 0), "cb_eval_points_host");
+  CB_CUDA(cudaStreamWaitEvent(p->down, p->start, 0), "cb_eval_points_host");
+  for (long long c = 0; c < nch; ++c) {
+    const long long b = c * per, m = (b + per <= M) ? per : M - b;
+    if (m <= 0) break;
+    CB_CUDA(cudaMemcpyAsync(d_points_ws + b * J, h_points + b * J, sizeof(double) * m * J, cudaMemcpyHostToDevice,
+                            p->up),
+            "cb_eval_points_host");
+    CB_CUDA(cudaEventRecord(p->landed[c], p->up), "cb_eval_points_host");
+    CB_CUDA(cudaStreamWaitEvent(s, p->landed[c], 0), "cb_eval_points_host");
+    CB_CUDA(eval_points(L, d_coef, m, d_points_ws + b * J, nullptr, d_out_ws + b, static_cast<Status*>(d_status),
+                        flags & 0xffff, s),
+            "cb_eval_points_host");
+    CB_CUDA(cudaEventRecord(p->evaluated[c], s), "cb_eval_points_host");
+    CB_CUDA(cudaStreamWaitEvent(p->down, p->evaluated[c], 0), "cb_eval_points_host");
+    CB_CUDA(cudaMemcpyAsync(h_out + b, d_out_ws + b, sizeof(double) * m, cudaMemcpyDeviceToHost, p->down),
+            "cb_eval_points_host");
+  }
+  CB_CUDA(cudaEventRecord(p->done, p->down), "cb_eval_points_host");
+  CB_CUDA(cudaStreamWaitEvent(s, p->done, 0), "cb_eval_points_host");  // completion is ordered on `stream`
+  return CB_OK;
+}
+
 static int fill_advect(int J, const double* A, double dt, const double* lo, const double* hi, int source,
                        AdvectSpec& adv) {
   std::memset(&adv, 0, sizeof(adv));

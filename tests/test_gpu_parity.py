@@ -154,6 +154,34 @@ def test_eval_points_shard_bitwise_invariance(cuda):
         assert np.array_equal(part, full[a:b]), (a, b, float(np.abs(part - full[a:b]).max()))
 
 
+@pytest.mark.parametrize("cfg,M", [("2", 0), ("2", 1000), ("2", 600_000), ("4", 2_100_000), ("3", 300_007)])
+def test_eval_points_pinned_host_pipeline(cuda, cfg, M):
+    """Pinned host points go through cb_eval_points_host (chunked H2D / eval / D2H on copy
+    streams): bit-identical to the device-resident call, result in pinned host memory."""
+    import torch
+
+    if cfg == "3":
+        w = workloads.make("3")
+        points = 2.0 * np.random.default_rng(3).random((M, w.J)) - 1.0
+    else:
+        w = workloads.make(cfg, M=max(M, 1))
+        points = w.points[:M]
+    t = cn.tensor_coeffs(w.values, bases_for(w.J, w.n))
+    pts = torch.from_numpy(np.ascontiguousarray(points)).pin_memory()
+    got = cn.eval_points(t, pts)
+    assert isinstance(got, torch.Tensor) and not got.is_cuda and got.shape == (M,)
+    assert got.is_pinned() or M == 0  # (an empty tensor reports unpinned)
+    ref = cn.eval_points(t, pts.cuda()).cpu()
+    assert torch.equal(got, ref)
+    if M and M <= 1000:
+        close(got.numpy(), orc.eval_points(orc.tensor_coeffs(w.values), points))
+    if M:
+        bad = pts.clone().pin_memory()
+        bad[M // 2, 0] = 1.5
+        with pytest.raises(ValueError, match="beyond tolerance"):
+            cn.eval_points(t, bad)
+
+
 def test_polynomial_exactness(cuda):
     # T/test_chebnd.py:355-368 (seed 46): exact for polynomials of the basis degrees
     rng = np.random.default_rng(46)
