@@ -1,0 +1,273 @@
+// K2 row-contraction evaluator (q == 1, K <= 48): see the kernel comment below; launched by
+// eval_points() in cb_eval.cu.  Separate translation unit so its instantiations compile in
+// parallel with the k-contraction kernels.
+#include <cuda.h>
+#include "cb_common.cuh"
+#include "cb_eval_dev.cuh"
+#include "cb_kernels.h"
+
+namespace cb {
+namespace evk {
+namespace {
+
+// ------------------------------------------------------------------------------------------
+// Row-contraction form for small K (q == 1, K <= 48), e.g. BASELINE config 2 (33^3):
+//   U'[k][p] = sum_r A[r][k] W[r][p]   (DMMA: M = k (padded to 8*MTK), K-dim = rows, N = points)
+//   v[p]     = sum_k U'[k][p] T_k(x_{J-1,p})   (once per tile)
+// W[r][p] = prod_{leading d} T_{l_d(r)}(x_{d,p}) is formed on the fly as the B operand, so the
+// per-row weighting rides inside the tensor-core reduction and the accumulators are consumed
+// only once per tile (no per-stage epilogue / DMMA drain).
+// ------------------------------------------------------------------------------------------
+template <int NL, int MTK, int KT>
+__global__ void __launch_bounds__(Roles<16>::THREADS, 1)
+    eval_rc_kernel(const __grid_constant__ EvalParams p, const __grid_constant__ DmmaSmem sm,
+                   const __grid_constant__ CUtensorMap amap) {
+  constexpr int NCW = 16, NT = 2, kRows = 64;
+  constexpr int J = NL + 1;
+  constexpr int KTMAX = (KT < 0) ? 3 : KT;        // DFMA tail columns (compile-time when KT >= 0)
+  const int ktail = (KT < 0) ? p.ktail : KT;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* bar_full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* bar_empty = bar_full + kMaxStages;
+  uint64_t* tab_full = bar_empty + kMaxStages;
+  uint64_t* tab_empty = tab_full + 2;
+  double* Src = reinterpret_cast<double*>(smem_raw + sm.src);        // [ntab][P]
+  double* Red = reinterpret_cast<double*>(smem_raw + sm.red);        // [2][4][P]
+  double* Ts = reinterpret_cast<double*>(smem_raw + sm.ts);          // [ntab][ts_stride]
+  double* As = reinterpret_cast<double*>(smem_raw + sm.as);          // [stages][64][kc]
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const long long ntiles = (p.M + kP - 1) / kP;
+  if (tid == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&bar_full[s], 1);
+      mbar_init(&bar_empty[s], NCW);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tab_full[s], 1);
+      mbar_init(&tab_empty[s], NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == NCW) {  // producer
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&amap)) : "memory");
+      const unsigned stage_bytes = static_cast<unsigned>(kRows * p.kc * 8);
+      int slot = 0;
+      unsigned phase = 0;
+      for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int blk = 0; blk < p.nstage_blocks; ++blk) {
+          mbar_wait(&bar_empty[slot], phase ^ 1);
+          mbar_arrive_expect_tx(&bar_full[slot], stage_bytes);
+          tma_load_2d(As + static_cast<size_t>(slot) * kRows * p.kc, &amap, 0, blk * kRows, &bar_full[slot]);
+          if (++slot == p.stages) {
+            slot = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    return;
+  }
+  if (warp == NCW + 1) {  // builder: per-tile point tables
+    int it = 0;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int ts = it % sm.ntab;
+      mbar_wait(&tab_empty[ts], ((it / sm.ntab) & 1) ^ 1);
+      double* Tsb = Ts + ts * sm.ts_stride;
+      for (int pp = lane; pp < kP; pp += 32) {
+        const long long g = tile * kP + pp;
+        double t[kMaxDims];
+        double src = 0.0;
+        if (g < p.M) {
+          point_coords(p, g, t, &src);
+        } else {
+#pragma unroll
+          for (int d = 0; d < kMaxDims; ++d) t[d] = 0.0;
+        }
+        Src[ts * kP + pp] = src;
+#pragma unroll
+        for (int d = 0; d < J; ++d) {
+          double* col = Tsb + p.toff[d] + pp;
+          cheb_row(t[d], p.n[d], col, kTP);
+          for (int l = p.n[d]; l < p.trows[d]; ++l) col[l * kTP] = 0.0;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tab_full[ts]);
+    }
+    return;
+  }
+
+  // consumers: warp = (row group rg: 16 rows of each stage) x (point group ng: 16 points)
+  const int rg = warp >> 2, ng = warp & 3;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int pcol = ng * 16 + gq;  // B-fragment column (point) of this lane (+ nt*8)
+  const int R = static_cast<int>(p.R);
+  int slot = 0, it = 0;
+  unsigned phase = 0;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int ts = it % sm.ntab;
+    mbar_wait(&tab_full[ts], (it / sm.ntab) & 1);
+    const double* Tsb = Ts + ts * sm.ts_stride;
+    double acc[MTK][NT][2];
+#pragma unroll
+    for (int m = 0; m < MTK; ++m)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) acc[m][nt][0] = acc[m][nt][1] = 0.0;
+    double tacc[KTMAX > 0 ? KTMAX : 1][NT];
+#pragma unroll
+    for (int t = 0; t < KTMAX; ++t)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) tacc[t][nt] = 0.0;
+
+    for (int blk = 0; blk < p.nstage_blocks; ++blk) {
+      mbar_wait(&bar_full[slot], phase);
+      const double* Ast = As + static_cast<size_t>(slot) * kRows * p.kc + (rg * 16 + tq) * p.kc + gq;
+      // digits of this lane's first row r = blk*64 + rg*16 + tq (then r += 4 per k-step)
+      int r = blk * kRows + rg * 16 + tq;
+      int dig[NL];
+      {
+        uint32_t rem = static_cast<uint32_t>(r);
+#pragma unroll
+        for (int d = NL - 1; d >= 0; --d) {
+          uint32_t qd, l;
+          p.fdn[d].divmod(rem, qd, l);
+          dig[d] = static_cast<int>(l);
+          rem = qd;
+        }
+      }
+      const int kvalid = min(4, (static_cast<int>(p.R8) - (blk * kRows + rg * 16) + 3) / 4);  // k-steps with rows < R8
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        if (ks >= kvalid) break;
+        // B fragments: W[r][p] for this lane's row r and points pcol + 8*nt (zero past R)
+        double w[NT];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          double v = Tsb[p.toff[0] + dig[0] * kTP + pcol + nt * 8];
+#pragma unroll
+          for (int d = 1; d < NL; ++d) v *= Tsb[p.toff[d] + dig[d] * kTP + pcol + nt * 8];
+          w[nt] = (r < R) ? v : 0.0;
+        }
+        // A^T fragments: A[r][mt*8 + gq]
+        double a[MTK];
+#pragma unroll
+        for (int m = 0; m < MTK; ++m) a[m] = Ast[ks * 4 * p.kc + m * 8];
+#pragma unroll
+        for (int m = 0; m < MTK; ++m)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma884(acc[m][nt][0], acc[m][nt][1], a[m], w[nt]);
+        // tail columns k = 8*MTK + t (t < ktail) on DFMA: lane-partial sums over its rows
+#pragma unroll
+        for (int t = 0; t < KTMAX; ++t) {
+          if (t < ktail) {
+            const double at = Ast[ks * 4 * p.kc + MTK * 8 + t - gq];  // A[r][8*MTK + t] (broadcast in tq)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) tacc[t][nt] = fma(at, w[nt], tacc[t][nt]);
+          }
+        }
+        // advance the row digits by 4 (last leading mode fastest; n >= 1)
+        r += 4;
+        dig[NL - 1] += 4;
+#pragma unroll
+        for (int d = NL - 1; d >= 1; --d) {
+          while (dig[d] >= p.n[d]) {
+            dig[d] -= p.n[d];
+            ++dig[d - 1];
+          }
+        }
+        if (dig[0] >= p.n[0]) dig[0] = p.n[0] - 1;  // r >= R: clamp the lookup (weight is zeroed)
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_empty[slot]);
+      if (++slot == p.stages) {
+        slot = 0;
+        phase ^= 1;
+      }
+    }
+    // tile end: contract k with T_k(x_{J-1}):  lane holds U'[k = m*8 + gq][p = ng*16 + nt*8 + 2tq + i]
+    double vp[NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int pp = ng * 16 + nt * 8 + 2 * tq + i;
+        double v = 0.0;
+#pragma unroll
+        for (int m = 0; m < MTK; ++m) v = fma(acc[m][nt][i], Tsb[p.toff[J - 1] + (m * 8 + gq) * kTP + pp], v);
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        vp[nt][i] = v;
+      }
+    // tail columns: reduce the row-partials over the 4 tq lanes -> U'[8*MTK + t][p = pcol + 8*nt]
+    double tv[NT] = {};
+#pragma unroll
+    for (int t = 0; t < KTMAX; ++t) {
+      if (t < ktail) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          double u = tacc[t][nt];
+          u += __shfl_xor_sync(0xffffffffu, u, 1);
+          u += __shfl_xor_sync(0xffffffffu, u, 2);
+          tv[nt] = fma(u, Tsb[p.toff[J - 1] + (MTK * 8 + t) * kTP + pcol + nt * 8], tv[nt]);
+        }
+      }
+    }
+    double* Rb = Red + (it & 1) * 8 * kP;  // [2][rg: 4 main + 4 tail][P]
+    if (gq == 0) {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) Rb[rg * kP + ng * 16 + nt * 8 + 2 * tq + i] = vp[nt][i];
+    }
+    if (tq == 0) {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) Rb[(4 + rg) * kP + pcol + nt * 8] = tv[nt];
+    }
+    consumer_sync_n(NCW * 32);
+    if (tid < kP) {
+      const long long g = tile * kP + tid;
+      if (g < p.M) {
+        double v = ((Rb[tid] + Rb[kP + tid]) + Rb[2 * kP + tid]) + Rb[3 * kP + tid];
+        if (KTMAX > 0 && ktail) v += ((Rb[4 * kP + tid] + Rb[5 * kP + tid]) + Rb[6 * kP + tid]) + Rb[7 * kP + tid];
+        p.out[g] = v - Src[ts * kP + tid];
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&tab_empty[ts]);
+  }
+}
+
+}  // namespace
+
+bool launch_eval_rc(int NL, int MTK, int KT, unsigned grid, size_t bytes, cudaStream_t stream, const EvalParams& p,
+                    const DmmaSmem& sm, const CUtensorMap& amap) {
+  // exact tail instantiations for J <= 4 (the common shapes); runtime tail above
+  const int kt = (NL <= 3) ? KT : -1;
+  switch ((NL * 8 + MTK) * 8 + (kt + 1)) {
+#define CB_RC(v, m, t)                                                                                    \
+  case (v * 8 + m) * 8 + (t + 1):                                                                         \
+    ensure_smem_attr(reinterpret_cast<const void*>(eval_rc_kernel<v, m, t>), 227 * 1024);                 \
+    eval_rc_kernel<v, m, t><<<grid, Roles<16>::THREADS, bytes, stream>>>(p, sm, amap);                    \
+    return true;
+#define CB_RCT(v, m) CB_RC(v, m, 0) CB_RC(v, m, 1) CB_RC(v, m, 2) CB_RC(v, m, 3)
+#define CB_RCM(v, X) X(v, 1) X(v, 2) X(v, 3) X(v, 4) X(v, 5) X(v, 6)
+#define CB_RCR(v, m) CB_RC(v, m, -1)
+    CB_RCM(1, CB_RCT) CB_RCM(2, CB_RCT) CB_RCM(3, CB_RCT)
+    CB_RCM(4, CB_RCR) CB_RCM(5, CB_RCR) CB_RCM(6, CB_RCR) CB_RCM(7, CB_RCR)
+#undef CB_RCR
+#undef CB_RCM
+#undef CB_RCT
+#undef CB_RC
+    default:
+      return false;
+  }
+}
+
+}  // namespace evk
+}  // namespace cb
