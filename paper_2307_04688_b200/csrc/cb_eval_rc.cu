@@ -127,23 +127,23 @@ __global__ void __launch_bounds__(Roles<16>::THREADS, 1)
     for (int blk = 0; blk < p.nstage_blocks; ++blk) {
       mbar_wait(&bar_full[slot], phase);
       const double* Ast = As + static_cast<size_t>(slot) * kRows * p.kc + (rg * 16 + tq) * p.kc + gq;
-      // digits of this lane's first row r = blk*64 + rg*16 + tq (then r += 4 per k-step)
-      int r = blk * kRows + rg * 16 + tq;
-      int dig[NL];
-      {
-        uint32_t rem = static_cast<uint32_t>(r);
+      const int rbase = blk * kRows + rg * 16 + tq;   // this lane's row at k-step ks: rbase + 4*ks
+      // one k-step: 4 rows of the stage; the row digits come straight from FastDiv (no carries),
+      // so the fully-valid case below is straight-line code the scheduler can software-pipeline
+      auto kstep = [&](int ks) {
+        const int r = rbase + 4 * ks;
+        int dig[NL];
+        {
+          uint32_t rem = static_cast<uint32_t>(r);
 #pragma unroll
-        for (int d = NL - 1; d >= 0; --d) {
-          uint32_t qd, l;
-          p.fdn[d].divmod(rem, qd, l);
-          dig[d] = static_cast<int>(l);
-          rem = qd;
+          for (int d = NL - 1; d >= 1; --d) {
+            uint32_t qd, l;
+            p.fdn[d].divmod(rem, qd, l);
+            dig[d] = static_cast<int>(l);
+            rem = qd;
+          }
+          dig[0] = min(static_cast<int>(rem), p.n[0] - 1);  // r >= R: clamp the lookup (weight is zeroed)
         }
-      }
-      const int kvalid = min(4, (static_cast<int>(p.R8) - (blk * kRows + rg * 16) + 3) / 4);  // k-steps with rows < R8
-#pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-        if (ks >= kvalid) break;
         // B fragments: W[r][p] for this lane's row r and points pcol + 8*nt (zero past R)
         double w[NT];
 #pragma unroll
@@ -170,17 +170,14 @@ __global__ void __launch_bounds__(Roles<16>::THREADS, 1)
             for (int nt = 0; nt < NT; ++nt) tacc[t][nt] = fma(at, w[nt], tacc[t][nt]);
           }
         }
-        // advance the row digits by 4 (last leading mode fastest; n >= 1)
-        r += 4;
-        dig[NL - 1] += 4;
+      };
+      const int kvalid = min(4, (static_cast<int>(p.R8) - (blk * kRows + rg * 16) + 3) / 4);  // k-steps with rows < R8
+      if (kvalid == 4) {
 #pragma unroll
-        for (int d = NL - 1; d >= 1; --d) {
-          while (dig[d] >= p.n[d]) {
-            dig[d] -= p.n[d];
-            ++dig[d - 1];
-          }
-        }
-        if (dig[0] >= p.n[0]) dig[0] = p.n[0] - 1;  // r >= R: clamp the lookup (weight is zeroed)
+        for (int ks = 0; ks < 4; ++ks) kstep(ks);
+      } else {
+#pragma unroll 1
+        for (int ks = 0; ks < kvalid; ++ks) kstep(ks);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_empty[slot]);
