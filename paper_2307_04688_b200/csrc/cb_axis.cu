@@ -243,7 +243,7 @@ struct Fused2Params {
   long long R;
 };
 
-constexpr int kF2RT = 16;      // r' per tile
+constexpr int kF2RT = 8;       // r' per tile
 constexpr int kF2Warps = 7;    // 7 x 32 = 224 >= 13 * 16 step-1 rows; 3 CTAs / SM
 constexpr int kF2Threads = kF2Warps * 32;
 constexpr int kF2IB = 5;       // K <= 25 (5 blocks)       // outputs per thread item (compile-time constant-bank indices)
@@ -278,7 +278,7 @@ __device__ __forceinline__ void f2_step2(const Fused2Params<N, K>& p, const doub
 }
 
 template <int N, int K>
-__global__ void __launch_bounds__(kF2Threads, 3) fused2_kernel(const __grid_constant__ Fused2Params<N, K> p) {
+__global__ void __launch_bounds__(kF2Threads, 6) fused2_kernel(const __grid_constant__ Fused2Params<N, K> p) {
   extern __shared__ __align__(16) double f2sm[];
   double* sX = f2sm;                   // [N*N][RT]
   double* sZ = f2sm + N * N * kF2RT;   // [N][RT][K]
