@@ -315,3 +315,39 @@ def test_advect_loop_config3_prefix(cuda):
     w = workloads.make("3", steps=3)
     got = cn.advect_loop(w.values, bases_for(w.J, w.n), w.A, w.dt, w.steps)
     close(got, orc.advect_loop(w.values, w.A, w.dt, w.steps))
+
+
+def test_config5b_stepwise_oracle(cuda):
+    """SURVEY §8(d) parity plan (i) for config 5b (J=6, n=13, full size): the GPU's V_t goes to the
+    host, the oracle builds it (tensor_coeffs) and evaluates a seeded subset of 1,024 advected
+    nodes; the GPU's V_{t+1} must match there, for t = 0 and t = 1."""
+    w = workloads.make("5b")
+    bases = bases_for(w.J, w.n)
+    T, S = orc.advect_points(w.values.shape, w.A, w.dt)
+    idx = np.sort(np.random.default_rng(55).choice(T.shape[0], 1024, replace=False))
+    V = w.values
+    for _ in range(2):
+        V_next = cn.advect_loop(V, bases, w.A, w.dt, 1)
+        ref = orc.eval_points(orc.tensor_coeffs(V), T[idx]) - S[idx]
+        close(V_next.ravel()[idx], ref)
+        V = V_next
+
+
+def test_config5b_reduced_full_loop(cuda):
+    """SURVEY §8(d) parity plan (ii): the full 20-step loop of config 5b at reduced n (J=6, n=5)."""
+    w = workloads.make("5b", n=5)
+    assert w.values.shape == (5,) * 6 and w.steps == 20
+    got = cn.advect_loop(w.values, bases_for(w.J, w.n), w.A, w.dt, w.steps)
+    close(got, orc.advect_loop(w.values, w.A, w.dt, w.steps))
+
+
+def test_config4_full_batch_subset(cuda):
+    """config 4 at its full M = 2^24 points on the GPU, checked against the oracle on a
+    seeded subset of 2^14 point indices."""
+    w = workloads.make("4")
+    assert w.points.shape == (1 << 24, 5)
+    t = cn.tensor_coeffs(w.values, bases_for(w.J, w.n))
+    got = cn.eval_points(t, w.points)
+    idx = np.sort(np.random.default_rng(44).choice(w.points.shape[0], 1 << 14, replace=False))
+    ref = orc.eval_points_parallel(orc.tensor_coeffs(w.values), w.points[idx])
+    close(got[idx], ref)
