@@ -575,7 +575,7 @@ def run_ours(args):
         achieved = bytes_alg / (t_total / args.steps) / 1e9
         roofline = {"bound": "hbm", "kernel": "eval_grid (K3 mode products)", "achieved": achieved,
                     "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-                    "algorithmic": "8*(n^J + k^J) bytes per step", "traffic": ncu_traffic("rotate_fixed", cfg)}
+                    "algorithmic": "8*(n^J + k^J) bytes per step", "traffic": ncu_traffic("eval_grid", cfg)}
         t0 = time.perf_counter()
         for _ in range(args.steps):
             res = cn.eval_grid(cn.tensor_coeffs(w.values, bases), targets)
