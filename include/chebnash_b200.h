@@ -36,8 +36,9 @@ extern "C" {
 
 enum {
   CB_OK = 0,
-  CB_EINVAL = 1,  /* bad shape / argument (reference raises ValueError) */
-  CB_ECUDA = 4    /* CUDA runtime error */
+  CB_EINVAL = 1,     /* bad shape / argument (reference raises ValueError) */
+  CB_ENONFINITE = 2, /* non-finite objective sample in a Bellman sweep (FloatingPointError) */
+  CB_ECUDA = 4       /* CUDA runtime error */
 };
 
 int cb_abi_version(void);
@@ -151,6 +152,58 @@ int cb_gather_take(int ndim_in, const int64_t* shape_in, const double* d_in, int
 int64_t cb_eval_grid_workspace(int J, const int64_t* n, const int64_t* k);
 int cb_eval_grid(int J, const int64_t* n, const double* d_coef, const int64_t* k, const double* const* d_E,
                  double* d_out, double* d_work, int64_t work_elems, void* stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * Collocation solver: the Bellman sweep of solver.py on the device.
+ * ------------------------------------------------------------------------------------------- */
+#define CB_MAX_PLAYERS 8
+#define CB_MAX_CONTROL_NODES 32
+
+/* GameSpec (game.py:29-107) + the derived constants a sweep needs.  Node enumeration of the
+ * state grid is dimension 1 fastest (game.py:117-126): node p has coordinates nodes[p*J + d]. */
+typedef struct {
+  int J;                                   /* players = state dimensions, 2..8 */
+  int np[CB_MAX_PLAYERS];                  /* state nodes per dimension, Np_d + 1 (2..64) */
+  int nu[CB_MAX_PLAYERS];                  /* control nodes per player, Nu_i + 1 (2..32) */
+  double h, delta, P_max, U_max, tol;      /* Euler step, 1 - rho*h, boxes, stopping tolerance */
+  double A[CB_MAX_PLAYERS], phi[CB_MAX_PLAYERS];
+  double K[CB_MAX_PLAYERS][CB_MAX_PLAYERS];            /* exchange matrix (game.py:140-151) */
+  double beta[CB_MAX_PLAYERS], c[CB_MAX_PLAYERS], m[CB_MAX_PLAYERS];
+  double unodes[CB_MAX_PLAYERS][CB_MAX_CONTROL_NODES]; /* make_basis(Nu_i, 0, U_max).nodes */
+  double rnodes[CB_MAX_PLAYERS][CB_MAX_CONTROL_NODES]; /* reference_nodes(Nu_i) */
+} cb_game_t;
+
+/* One synchronous best-response sweep over all players and nodes: _run_sweep + _best_response_block
+ * (solver.py:359-438), one warp per (player, node).
+ *   d_nodes  (N_P, J) state nodes;  d_stacks: J drift stacks (precompute_dynamics_stack,
+ *            solver.py:141-159), each (nu_1, ..., nu_J, N_P) C-order, concatenated;
+ *   d_coef   (J, N_P) value coefficients of the current fields, player i's tensor stored with
+ *            REVERSED axes (l_J, ..., l_1) — exactly cb_transform_axes over axes 1..J of the node
+ *            values viewed as (J, np_J, ..., np_1), i.e. _refit (solver.py:441-449) without a copy;
+ *   d_v, d_u (J, N_P) current values / policy -> d_v_out, d_u_out (J, N_P);
+ *   d_clamped: uint64 counter, incremented by the number of clamped successor components.
+ * A non-finite objective sets d_status->nonfinite (FloatingPointError, solver.py:400-401). */
+int cb_bellman_sweep(const cb_game_t* game, const double* d_nodes, const double* d_stacks, const double* d_coef,
+                     const double* d_v, const double* d_u, double* d_v_out, double* d_u_out, uint64_t* d_clamped,
+                     void* d_status, void* stream);
+
+/* Device work bytes for cb_solve (history + clamp counts + control block). */
+int64_t cb_solve_work_bytes(const cb_game_t* game, int64_t max_iters);
+
+/* Fixed-point driver `solve` (solver.py:495-570) run on the device: sweeps + refits captured in
+ * CUDA graphs, convergence tested on the device (sup-norm change < tol), no host work per sweep.
+ * d_v, d_u, d_coef each hold TWO (J, N_P) buffers; the initial fields are in buffer 0.  On return
+ * the final fields are in buffer (*iterations % 2).  d_work layout (cb_solve_work_bytes):
+ *   [max_iters * J doubles: per-sweep per-player sup change][max_iters uint64: clamp counts][ctl].
+ * Returns CB_ENONFINITE if a sweep produced a non-finite objective (*iterations = that sweep). */
+int cb_solve(const cb_game_t* game, const double* d_nodes, const double* d_stacks, double* d_v, double* d_u,
+             double* d_coef, void* d_work, int64_t max_iters, int64_t* iterations, int* converged, void* stream);
+
+/* Safeguarded maximiser _maximise_block (solver.py:262-323) on m rows of L coefficients
+ * (reference variable on [-1, 1]) from warm starts d_x0: d_x, d_f (m,).  always_scan != 0 adds the
+ * dense-scan candidate for every row (newton_maximize, solver.py:326-356). */
+int cb_maximise_rows(int64_t m, int L, const double* d_coef, const double* d_x0, double* d_x, double* d_f,
+                     int always_scan, void* stream);
 
 #ifdef __cplusplus
 }

@@ -23,6 +23,35 @@ _vp = ctypes.c_void_p
 _i64p = ctypes.POINTER(ctypes.c_int64)
 _dblp = ctypes.POINTER(ctypes.c_double)
 
+MAX_PLAYERS = 8          # CB_MAX_PLAYERS
+MAX_CONTROL_NODES = 32   # CB_MAX_CONTROL_NODES
+
+
+class CbGame(ctypes.Structure):
+    """cb_game_t (include/chebnash_b200.h): GameSpec + derived node tables for the device solver."""
+
+    _fields_ = [
+        ("J", ctypes.c_int),
+        ("np", ctypes.c_int * MAX_PLAYERS),
+        ("nu", ctypes.c_int * MAX_PLAYERS),
+        ("h", ctypes.c_double),
+        ("delta", ctypes.c_double),
+        ("P_max", ctypes.c_double),
+        ("U_max", ctypes.c_double),
+        ("tol", ctypes.c_double),
+        ("A", ctypes.c_double * MAX_PLAYERS),
+        ("phi", ctypes.c_double * MAX_PLAYERS),
+        ("K", (ctypes.c_double * MAX_PLAYERS) * MAX_PLAYERS),
+        ("beta", ctypes.c_double * MAX_PLAYERS),
+        ("c", ctypes.c_double * MAX_PLAYERS),
+        ("m", ctypes.c_double * MAX_PLAYERS),
+        ("unodes", (ctypes.c_double * MAX_CONTROL_NODES) * MAX_PLAYERS),
+        ("rnodes", (ctypes.c_double * MAX_CONTROL_NODES) * MAX_PLAYERS),
+    ]
+
+
+_gamep = ctypes.POINTER(CbGame)
+
 # name -> (restype, argtypes); must match include/chebnash_b200.h
 SIGNATURES = {
     "cb_abi_version": (_c_int, []),
@@ -50,6 +79,10 @@ SIGNATURES = {
     "cb_gather_take": (_c_int, [_c_int, _i64p, _vp, _c_i64, _vp, _c_int, _i64p, _vp, _vp]),
     "cb_eval_grid_workspace": (_c_i64, [_c_int, _i64p, _i64p]),
     "cb_eval_grid": (_c_int, [_c_int, _i64p, _vp, _i64p, ctypes.POINTER(_vp), _vp, _vp, _c_i64, _vp]),
+    "cb_bellman_sweep": (_c_int, [_gamep, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "cb_solve_work_bytes": (_c_i64, [_gamep, _c_i64]),
+    "cb_solve": (_c_int, [_gamep, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _i64p, ctypes.POINTER(_c_int), _vp]),
+    "cb_maximise_rows": (_c_int, [_c_i64, _c_int, _vp, _vp, _vp, _vp, _c_int, _vp]),
 }
 
 _lib = None
@@ -86,6 +119,8 @@ def check(rc: int, what: str = "") -> None:
         msg = load().cb_last_error().decode(errors="replace")
         if rc == 1:
             raise ValueError(msg or what)
+        if rc == 2:
+            raise FloatingPointError(msg or what)
         raise CudaLibraryError(f"{what}: {msg}" if what else msg)
 
 

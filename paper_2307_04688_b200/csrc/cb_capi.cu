@@ -452,3 +452,63 @@ int cb_eval_grid(int J, const int64_t* n, const double* d_coef, const int64_t* k
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------------------------
+// collocation solver (cb_solver.cu)
+// ---------------------------------------------------------------------------------------------
+static int check_game(const cb_game_t* g, const char* fn) {
+  if (!g) return fail(CB_EINVAL, std::string(fn) + ": null game");
+  if (g->J < 2 || g->J > CB_MAX_PLAYERS) return fail(CB_EINVAL, std::string(fn) + ": need 2..8 players");
+  long long nodes = 1;
+  for (int d = 0; d < g->J; ++d) {
+    if (g->np[d] < 2 || g->np[d] > 64) return fail(CB_EINVAL, std::string(fn) + ": state degree must be 1..63");
+    if (g->nu[d] < 2 || g->nu[d] > CB_MAX_CONTROL_NODES)
+      return fail(CB_EINVAL, std::string(fn) + ": control degree must be 1..31");
+    nodes *= g->np[d];
+    if (nodes > (1LL << 31)) return fail(CB_EINVAL, std::string(fn) + ": state grid too large");
+  }
+  if (!(g->P_max > 0) || !(g->U_max > 0) || !(g->h > 0))
+    return fail(CB_EINVAL, std::string(fn) + ": boxes and step must be positive");
+  return CB_OK;
+}
+
+int cb_bellman_sweep(const cb_game_t* game, const double* d_nodes, const double* d_stacks, const double* d_coef,
+                     const double* d_v, const double* d_u, double* d_v_out, double* d_u_out, uint64_t* d_clamped,
+                     void* d_status, void* stream) {
+  int rc = check_game(game, "cb_bellman_sweep");
+  if (rc) return rc;
+  CB_CUDA(bellman_sweep(*game, d_nodes, d_stacks, d_coef, d_v, d_u, d_v_out, d_u_out,
+                        reinterpret_cast<unsigned long long*>(d_clamped), static_cast<Status*>(d_status),
+                        static_cast<cudaStream_t>(stream)),
+          "cb_bellman_sweep");
+  return CB_OK;
+}
+
+int64_t cb_solve_work_bytes(const cb_game_t* game, int64_t max_iters) {
+  if (check_game(game, "cb_solve_work_bytes") || max_iters < 1) return -1;
+  return solve_work_bytes(*game, max_iters);
+}
+
+int cb_solve(const cb_game_t* game, const double* d_nodes, const double* d_stacks, double* d_v, double* d_u,
+             double* d_coef, void* d_work, int64_t max_iters, int64_t* iterations, int* converged, void* stream) {
+  int rc = check_game(game, "cb_solve");
+  if (rc) return rc;
+  if (max_iters < 1) return fail(CB_EINVAL, "max_iters must be positive");
+  long long its = 0;
+  int conv = 0, nonfinite = 0;
+  CB_CUDA(solve(*game, d_nodes, d_stacks, d_v, d_u, d_coef, d_work, max_iters, &its, &conv, &nonfinite,
+                static_cast<cudaStream_t>(stream)),
+          "cb_solve");
+  *iterations = its;
+  *converged = conv;
+  if (nonfinite) return fail(CB_ENONFINITE, "non-finite objective sample in sweep");
+  return CB_OK;
+}
+
+int cb_maximise_rows(int64_t m, int L, const double* d_coef, const double* d_x0, double* d_x, double* d_f,
+                     int always_scan, void* stream) {
+  if (m < 0 || L < 1 || L > CB_MAX_CONTROL_NODES) return fail(CB_EINVAL, "cb_maximise_rows: need 1 <= L <= 32");
+  CB_CUDA(maximise_rows(m, L, d_coef, d_x0, d_x, d_f, always_scan, static_cast<cudaStream_t>(stream)),
+          "cb_maximise_rows");
+  return CB_OK;
+}

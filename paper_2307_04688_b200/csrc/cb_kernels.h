@@ -3,6 +3,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "cb_common.cuh"
+#include "../../include/chebnash_b200.h"
 
 namespace cb {
 
@@ -63,5 +64,16 @@ cudaError_t gather_take_f(int ndim_in, const long long* shape_in, const double* 
 cudaError_t eval_grid(const EvalLayout& L, const double* coef, const long long* k, const double* const* E,
                       double* out, double* work, long long work_elems, cudaStream_t stream);
 long long eval_grid_work_elems(const EvalLayout& L, const long long* k);
+
+// Collocation solver (cb_solver.cu).
+cudaError_t bellman_sweep(const cb_game_t& g, const double* nodes, const double* stacks, const double* coef,
+                          const double* v, const double* u, double* v_out, double* u_out,
+                          unsigned long long* clamped, Status* st, cudaStream_t stream);
+long long solve_work_bytes(const cb_game_t& g, long long max_iters);
+cudaError_t solve(const cb_game_t& g, const double* nodes, const double* stacks, double* v, double* u, double* coef,
+                  void* work, long long max_iters, long long* iterations, int* converged, int* nonfinite,
+                  cudaStream_t stream);
+cudaError_t maximise_rows(long long m, int L, const double* coef, const double* x0, double* x, double* f,
+                          int always_scan, cudaStream_t stream);
 
 }  // namespace cb

@@ -1,0 +1,593 @@
+// Collocation solver on the device: the Bellman sweep, the safeguarded
+// Newton maximiser and the fixed-point driver of the reference solver (S/solver.py).
+//
+// One warp per (player i, state node p) runs the whole best response of _best_response_block
+// (S/solver.py:359-409) for that node:
+//   1. bind the other players' current controls in the control-space drift stacks
+//      (Step 1, :374-379) -> the drift polynomial in the player's own control, (K, J);
+//   2. drift at the K own-control nodes, Euler successor, clip to the state box, clamp count
+//      (:382-386), one lane per own-control node;
+//   3. the player's value interpolant at the successor (:389-397) — nested accumulation over the
+//      state modes, dim 1 innermost, exactly the reference's binding order;
+//   4. objective delta*(stage + v) (:399-401), the 1-D fit M0 @ objective (:404);
+//   5. _maximise_block (:262-323): projected Newton on f', endpoints, and the 257-point scan +
+//      60-step bisection fallback (the scan spread over the 32 lanes).
+// The per-row maximiser follows numpy's arithmetic operation for operation (this file is
+// compiled with -fmad=false; numpy's pairwise summation is reproduced), so on identical
+// coefficient rows it is bitwise identical to the reference (tested).
+//
+// The driver (`solve`, :495-570) captures [sweep -> refit (K1 transform) -> convergence test]
+// pairs in a CUDA graph; the sup-norm change per player is reduced with atomicMax on the IEEE bits
+// (non-negative doubles order like their bit patterns) and the stopping test runs on the device,
+// so the host only polls a flag once per graph launch.
+#include <cstdio>
+#include <cmath>
+#include "../../include/chebnash_b200.h"
+#include "cb_common.cuh"
+#include "cb_kernels.h"
+
+namespace cb {
+
+namespace {
+
+constexpr int kSweepWarps = 4;
+constexpr int kSolverMaxJ = CB_MAX_PLAYERS;
+constexpr int kKMax = CB_MAX_CONTROL_NODES;
+constexpr int kScanPoints = 257;   // S/solver.py:52
+constexpr int kBisect = 60;        // :53
+constexpr int kNewtonIter = 30;    // :50
+constexpr double kNewtonTol = 1e-12;  // :51
+
+struct SolveCtl {
+  long long it;          // next sweep index (0-based)
+  long long max_iters;
+  long long iterations;  // set when done
+  int done;
+  int converged;
+  unsigned err;          // non-finite objective seen
+  int pad;
+};
+
+struct SweepArgs {
+  cb_game_t g;
+  long long NP;
+  const double* nodes;
+  const double* stacks;
+  long long stack_elems;  // prod(nu) * NP per stack
+  const double* coef;
+  const double* v_old;
+  const double* u_old;
+  double* v_new;
+  double* u_new;
+  unsigned long long* clamp;      // single-sweep counter (solve: clamp_base[it])
+  unsigned long long* hist_base;  // solve only: (max_iters, J) sup changes as IEEE bits
+  unsigned long long* clamp_base;
+  SolveCtl* ctl;                  // solve only
+  Status* st;                     // single sweep: non-finite flag
+};
+
+// numpy's pairwise summation for n <= 128 (umath loops: 8 partial sums, then a fixed tree).
+__device__ double np_sum(const double* a, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = r + a[i];
+    return r;
+  }
+  double r[8];
+  for (int j = 0; j < 8; ++j) r[j] = a[j];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
+    for (int j = 0; j < 8; ++j) r[j] = r[j] + a[i + j];
+  double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; i < n; ++i) res = res + a[i];
+  return res;
+}
+
+// _clenshaw_last (S/solver.py:226-236) for one row.
+__device__ double clenshaw_row(const double* c, int L, double x) {
+  if (L == 1) return c[0];
+  const double x2 = 2.0 * x;
+  double b1 = 0.0, b2 = 0.0;
+  for (int k = L - 1; k >= 1; --k) {
+    const double t = c[k] + x2 * b1 - b2;
+    b2 = b1;
+    b1 = t;
+  }
+  return c[0] + x * b1 - b2;
+}
+
+// derivative_array (S/cheb1d.py:230-249): p (L) -> q (L-1)
+__device__ void deriv_row(const double* p, int L, double* q) {
+  const int n = L - 1;
+  q[n - 1] = 2.0 * n * p[n];
+  if (n >= 2) q[n - 2] = 2.0 * (n - 1) * p[n - 1];
+  for (int l = n - 3; l >= 0; --l) q[l] = q[l + 2] + 2.0 * (l + 1) * p[l + 1];
+  q[0] *= 0.5;
+}
+
+__device__ __forceinline__ double np_sign(double v) { return v > 0.0 ? 1.0 : (v < 0.0 ? -1.0 : (v == 0.0 ? 0.0 : v)); }
+__device__ __forceinline__ double clip1(double v) { return fmin(fmax(v, -1.0), 1.0); }
+
+// _maximise_block for one row held in shared memory (c, L); all 32 lanes call it and get the
+// same (x, f).  q1 / q2: per-warp scratch (L-1, L-2).
+__device__ void warp_maximise(const double* c, int L, double x0, bool always_scan, double* q1, double* q2,
+                              double& x_out, double& f_out) {
+  const int lane = threadIdx.x & 31;
+  double alt[kKMax];
+  for (int l = 0; l < L; ++l) alt[l] = (l & 1) ? -c[l] : c[l];
+  const double f_hi = np_sum(c, L);
+  const double f_lo = np_sum(alt, L);
+  if (L <= 2) {
+    x_out = (f_hi >= f_lo) ? 1.0 : -1.0;
+    f_out = fmax(f_hi, f_lo);
+    return;
+  }
+  if (lane == 0) {
+    deriv_row(c, L, q1);
+    deriv_row(q1, L - 1, q2);
+  }
+  __syncwarp();
+  double x = clip1(x0);
+  bool moving = true, failed = false;
+  for (int it = 0; it < kNewtonIter; ++it) {
+    const double f1 = clenshaw_row(q1, L - 1, x);
+    const double f2 = clenshaw_row(q2, L - 2, x);
+    const bool tiny = fabs(f2) <= 1e-300;
+    const double raw = x - f1 / (tiny ? 1.0 : f2);
+    const double xn = clip1(raw);
+    if (moving && ((!tiny && raw != xn) || tiny)) failed = true;
+    moving = moving && !tiny;
+    const double dx = fabs(xn - x);
+    if (moving) x = xn;
+    moving = moving && (dx > kNewtonTol);
+    if (!moving) break;
+  }
+  failed = failed || moving;
+  failed = failed || (clenshaw_row(q2, L - 2, x) >= 0.0);
+  if (always_scan) failed = true;
+  double best_x = x, best_f = clenshaw_row(c, L, x);
+  if (f_lo > best_f) {
+    best_x = -1.0;
+    best_f = f_lo;
+  }
+  if (f_hi > best_f) {
+    best_x = 1.0;
+    best_f = f_hi;
+  }
+  if (failed) {
+    // dense scan over linspace(-1, 1, 257) (exact binary fractions), first maximum wins
+    double bv = -INFINITY;
+    int bj = kScanPoints;
+    for (int j = lane; j < kScanPoints; j += 32) {
+      const double xs = (j == kScanPoints - 1) ? 1.0 : -1.0 + j * (2.0 / (kScanPoints - 1));
+      const double v = clenshaw_row(c, L, xs);
+      if (v > bv || bj == kScanPoints) {
+        bv = v;
+        bj = j;
+      }
+    }
+    for (int o = 16; o >= 1; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+      if (ov > bv || (ov == bv && oj < bj)) {
+        bv = ov;
+        bj = oj;
+      }
+    }
+    auto xs_at = [](int j) { return (j == kScanPoints - 1) ? 1.0 : -1.0 + j * (2.0 / (kScanPoints - 1)); };
+    const double x_scan = xs_at(bj);
+    double lo = xs_at(bj > 0 ? bj - 1 : 0);
+    double hi = xs_at(bj < kScanPoints - 1 ? bj + 1 : kScanPoints - 1);
+    const double s_lo = np_sign(clenshaw_row(q1, L - 1, lo));
+    for (int s = 0; s < kBisect; ++s) {
+      const double mid = 0.5 * (lo + hi);
+      const bool same = np_sign(clenshaw_row(q1, L - 1, mid)) == s_lo;
+      if (same) lo = mid;
+      else hi = mid;
+    }
+    const double x_ref = 0.5 * (lo + hi);
+    const double x_fb = (clenshaw_row(c, L, x_ref) >= bv) ? x_ref : x_scan;
+    double cf = clenshaw_row(c, L, x_fb);
+    if (cf > best_f) {
+      best_x = x_fb;
+      best_f = cf;
+    }
+    cf = clenshaw_row(c, L, x_scan);
+    if (cf > best_f) {
+      best_x = x_scan;
+      best_f = cf;
+    }
+  }
+  x_out = best_x;
+  f_out = best_f;
+}
+
+// Value interpolant of one player at a point: coefficients with reversed axes (l_J, ..., l_1),
+// i.e. dim 0 is the memory-fastest axis; nested accumulation, dim 0 innermost.
+__device__ double eval_reversed(const double* C, int J, const int* np, const double* pt) {
+  double x2[kSolverMaxJ], t[kSolverMaxJ], tp[kSolverMaxJ], acc[kSolverMaxJ];
+  int dig[kSolverMaxJ];
+  long long total = 1;
+  for (int d = 0; d < J; ++d) {
+    x2[d] = 2.0 * pt[d];
+    t[d] = 1.0;
+    tp[d] = pt[d];  // T_{-1} := x so that T_1 = 2x*T_0 - T_{-1} = x
+    acc[d] = 0.0;
+    dig[d] = 0;
+    total *= np[d];
+  }
+  for (long long e = 0; e < total; ++e) {
+    acc[0] = acc[0] + C[e] * t[0];
+    const double tn = x2[0] * t[0] - tp[0];
+    tp[0] = t[0];
+    t[0] = tn;
+    if (++dig[0] == np[0]) {
+      for (int L = 0; L + 1 < J; ++L) {
+        if (dig[L] != np[L]) break;
+        dig[L] = 0;
+        t[L] = 1.0;
+        tp[L] = 0.5 * x2[L];
+        acc[L + 1] = acc[L + 1] + acc[L] * t[L + 1];
+        acc[L] = 0.0;
+        const double tn2 = x2[L + 1] * t[L + 1] - tp[L + 1];
+        tp[L + 1] = t[L + 1];
+        t[L + 1] = tn2;
+        ++dig[L + 1];
+      }
+    }
+  }
+  return acc[J - 1];
+}
+
+__global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(const __grid_constant__ SweepArgs a) {
+  __shared__ double sT[kSweepWarps][kSolverMaxJ - 1][kKMax];   // bound players' basis rows
+  __shared__ double sAcc[kSweepWarps][kKMax * kSolverMaxJ];      // drift polynomial (K, J)
+  __shared__ double sObj[kSweepWarps][kKMax];
+  __shared__ double sCoef[kSweepWarps][kKMax];
+  __shared__ double sQ1[kSweepWarps][kKMax];
+  __shared__ double sQ2[kSweepWarps][kKMax];
+  const cb_game_t& g = a.g;
+  const int J = g.J;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long task = static_cast<long long>(blockIdx.x) * kSweepWarps + warp;
+  if (task >= J * a.NP) return;
+  const int i = static_cast<int>(task / a.NP);
+  const long long p = task - static_cast<long long>(i) * a.NP;
+  const long long ip = static_cast<long long>(i) * a.NP + p;
+
+  long long it = 0;
+  if (a.ctl) {
+    if (a.ctl->done) {  // converged earlier in this graph launch: carry the fields forward
+      if (lane == 0) {
+        a.v_new[ip] = a.v_old[ip];
+        a.u_new[ip] = a.u_old[ip];
+      }
+      return;
+    }
+    it = a.ctl->it;
+  }
+  const int K = g.nu[i];
+  const double u_scale = 2.0 / g.U_max;
+  const double p_scale = 2.0 / g.P_max;
+
+  // 1. basis rows of the bound players' current controls at this node (Step 1, :374-379)
+  int bsz[kSolverMaxJ - 1], bdim[kSolverMaxJ - 1];
+  long long NB = 1;
+  for (int t = 0; t < J - 1; ++t) {
+    bdim[t] = t < i ? t : t + 1;
+    bsz[t] = g.nu[bdim[t]];
+    NB *= bsz[t];
+  }
+  if (lane < J - 1) {
+    const double x = a.u_old[static_cast<long long>(bdim[lane]) * a.NP + p] * u_scale - 1.0;
+    double* row = sT[warp][lane];
+    row[0] = 1.0;
+    if (bsz[lane] > 1) row[1] = x;
+    const double x2 = 2.0 * x;
+    for (int l = 2; l < bsz[lane]; ++l) row[l] = x2 * row[l - 1] - row[l - 2];
+  }
+  __syncwarp();
+  // stack strides (C order over (nu_1, ..., nu_J), then the node axis)
+  long long stride[kSolverMaxJ];
+  {
+    long long s = 1;
+    for (int d = J - 1; d >= 0; --d) {
+      stride[d] = s;
+      s *= g.nu[d];
+    }
+  }
+  // 2. bind: acc[l_own * J + comp] = sum over bound tuples of prod T * stack_comp[...]
+  for (int r = lane; r < K * J; r += 32) {
+    const int lown = r / J, comp = r - (r / J) * J;
+    const double* S = a.stacks + static_cast<long long>(comp) * a.stack_elems;
+    double acc = 0.0;
+    for (long long b = 0; b < NB; ++b) {
+      long long rem = b, off = static_cast<long long>(lown) * stride[i];
+      double w = 1.0;
+      int tt[kSolverMaxJ - 1];
+      for (int t = J - 2; t >= 0; --t) {
+        const long long q = rem / bsz[t];
+        tt[t] = static_cast<int>(rem - q * bsz[t]);
+        rem = q;
+        off += tt[t] * stride[bdim[t]];
+      }
+      for (int t = 0; t < J - 1; ++t) w = (t == 0) ? sT[warp][0][tt[0]] : w * sT[warp][t][tt[t]];
+      acc = acc + w * S[off * a.NP + p];
+    }
+    sAcc[warp][r] = acc;
+  }
+  __syncwarp();
+  // 3. own-control node k = lane: drift, successor, value, objective
+  unsigned clamped = 0;
+  if (lane < K) {
+    const int k = lane;
+    const double rn = g.rnodes[i][k];
+    double gk[kSolverMaxJ];
+    for (int c = 0; c < J; ++c) gk[c] = 0.0;
+    double T0 = 1.0, T1 = rn;
+    for (int l = 0; l < K; ++l) {
+      const double Tl = (l == 0) ? 1.0 : (l == 1 ? rn : (2.0 * rn) * T1 - T0);
+      if (l >= 2) {
+        T0 = T1;
+        T1 = Tl;
+      }
+      for (int c = 0; c < J; ++c) gk[c] = gk[c] + Tl * sAcc[warp][l * J + c];
+    }
+    double pt[kSolverMaxJ];
+    for (int c = 0; c < J; ++c) {
+      const double nxt = a.nodes[p * J + c] + g.h * gk[c];
+      const double cl = fmin(fmax(nxt, 0.0), g.P_max);
+      clamped += (cl != nxt) ? 1u : 0u;
+      pt[c] = cl * p_scale - 1.0;
+    }
+    const double vnext = eval_reversed(a.coef + static_cast<long long>(i) * a.NP, J, g.np, pt);
+    const double un = g.unodes[i][k];
+    const double gain = un * (g.A[i] - 0.5 * un);
+    const double xi = a.nodes[p * J + i];
+    const double damage = 0.5 * g.phi[i] * (xi * xi);
+    const double stage = g.h * (gain - damage);
+    const double obj = g.delta * (stage + vnext);
+    if (!isfinite(obj)) {
+      if (a.ctl) atomicOr(&a.ctl->err, 1u);
+      if (a.st) atomicOr(&a.st->nonfinite, 1u);
+    }
+    sObj[warp][k] = obj;
+  }
+  __syncwarp();
+  // 4. 1-D fit in the own control: coef_l = sum_k M0[l][k] obj_k, M0 = diag(s) B^T diag(w)
+  if (lane < K) {
+    const int l = lane, n = K - 1;
+    const double s = (l == 0 || l == n) ? 1.0 / n : 2.0 / n;
+    double acc = 0.0;
+    for (int k = 0; k < K; ++k) {
+      const double rn = g.rnodes[i][k];
+      double Tl = 1.0;
+      if (l >= 1) {
+        double t0 = 1.0, t1 = rn;
+        const double r2 = 2.0 * rn;
+        for (int m = 2; m <= l; ++m) {
+          const double tn = r2 * t1 - t0;
+          t0 = t1;
+          t1 = tn;
+        }
+        Tl = t1;
+      }
+      const double w = (k == 0 || k == n) ? 0.5 : 1.0;
+      acc = acc + (s * (Tl * w)) * sObj[warp][k];
+    }
+    sCoef[warp][l] = acc;
+  }
+  __syncwarp();
+  // 5. maximise from the warm start
+  double xb, fb;
+  warp_maximise(sCoef[warp], K, a.u_old[ip] * u_scale - 1.0, false, sQ1[warp], sQ2[warp], xb, fb);
+  for (int o = 16; o >= 1; o >>= 1) clamped += __shfl_xor_sync(0xffffffffu, clamped, o);
+  if (lane == 0) {
+    a.u_new[ip] = (xb + 1.0) * (0.5 * g.U_max);
+    a.v_new[ip] = fb;
+    unsigned long long* cl = a.ctl ? a.clamp_base + it : a.clamp;
+    if (cl && clamped) atomicAdd(cl, static_cast<unsigned long long>(clamped));
+    if (a.ctl) {
+      const double d = fabs(fb - a.v_old[ip]);
+      atomicMax(a.hist_base + it * J + i, static_cast<unsigned long long>(__double_as_longlong(d)));
+    }
+  }
+}
+
+__global__ void solve_init_kernel(SolveCtl* ctl, long long max_iters) {
+  ctl->it = 0;
+  ctl->max_iters = max_iters;
+  ctl->iterations = 0;
+  ctl->done = 0;
+  ctl->converged = 0;
+  ctl->err = 0;
+}
+
+// stopping test of solve (:551-556): sup-norm change below tol -> converged
+__global__ void solve_finish_kernel(SolveCtl* ctl, const unsigned long long* hist_base, int J, double tol) {
+  if (ctl->done) return;
+  const long long it = ctl->it;
+  ctl->it = it + 1;
+  if (ctl->err) {
+    ctl->done = 1;
+    ctl->iterations = it + 1;
+    return;
+  }
+  double dmax = 0.0;
+  for (int i = 0; i < J; ++i) dmax = fmax(dmax, __longlong_as_double(static_cast<long long>(hist_base[it * J + i])));
+  if (dmax < tol) {
+    ctl->done = 1;
+    ctl->converged = 1;
+    ctl->iterations = it + 1;
+  } else if (it + 1 >= ctl->max_iters) {
+    ctl->done = 1;
+    ctl->iterations = it + 1;
+  }
+}
+
+__global__ void maximise_rows_kernel(long long m, int L, const double* coef, const double* x0, double* x, double* f,
+                                     int always_scan) {
+  __shared__ double sC[kSweepWarps][kKMax];
+  __shared__ double sQ1[kSweepWarps][kKMax];
+  __shared__ double sQ2[kSweepWarps][kKMax];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long row = static_cast<long long>(blockIdx.x) * kSweepWarps + warp;
+  if (row >= m) return;
+  if (lane < L) sC[warp][lane] = coef[row * L + lane];
+  __syncwarp();
+  double xb, fb;
+  warp_maximise(sC[warp], L, x0[row], always_scan != 0, sQ1[warp], sQ2[warp], xb, fb);
+  if (lane == 0) {
+    x[row] = xb;
+    f[row] = fb;
+  }
+}
+
+long long nodes_of(const cb_game_t& g) {
+  long long n = 1;
+  for (int d = 0; d < g.J; ++d) n *= g.np[d];
+  return n;
+}
+
+long long stack_elems_of(const cb_game_t& g, long long NP) {
+  long long s = NP;
+  for (int d = 0; d < g.J; ++d) s *= g.nu[d];
+  return s;
+}
+
+cudaError_t launch_sweep(const SweepArgs& a, cudaStream_t s) {
+  const long long tasks = a.g.J * a.NP;
+  const long long blocks = (tasks + kSweepWarps - 1) / kSweepWarps;
+  sweep_kernel<<<static_cast<unsigned>(blocks), kSweepWarps * 32, 0, s>>>(a);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// refit (S/solver.py:441-449): node values (J, N_P) viewed as (J, np_J, ..., np_1) -> reversed-axis
+// coefficient tensors, one K1 transform over axes 1..J
+cudaError_t refit(const cb_game_t& g, const double* v, double* coef, cudaStream_t s) {
+  long long shape[kSolverMaxJ + 1];
+  shape[0] = g.J;
+  for (int d = 0; d < g.J; ++d) shape[1 + d] = g.np[g.J - 1 - d];
+  return transform_axes(g.J + 1, shape, 1, g.J + 1, v, coef, nullptr, 0, nullptr, s);
+}
+
+}  // namespace
+
+cudaError_t bellman_sweep(const cb_game_t& g, const double* nodes, const double* stacks, const double* coef,
+                          const double* v, const double* u, double* v_out, double* u_out,
+                          unsigned long long* clamped, Status* st, cudaStream_t stream) {
+  SweepArgs a{};
+  a.g = g;
+  a.NP = nodes_of(g);
+  a.nodes = nodes;
+  a.stacks = stacks;
+  a.stack_elems = stack_elems_of(g, a.NP);
+  a.coef = coef;
+  a.v_old = v;
+  a.u_old = u;
+  a.v_new = v_out;
+  a.u_new = u_out;
+  a.clamp = clamped;
+  a.st = st;
+  return launch_sweep(a, stream);
+}
+
+long long solve_work_bytes(const cb_game_t& g, long long max_iters) {
+  return max_iters * g.J * 8 + max_iters * 8 + 64;
+}
+
+cudaError_t solve(const cb_game_t& g, const double* nodes, const double* stacks, double* v, double* u, double* coef,
+                  void* work, long long max_iters, long long* iterations, int* converged, int* nonfinite,
+                  cudaStream_t stream) {
+  const long long NP = nodes_of(g);
+  const long long JN = g.J * NP;
+  unsigned long long* hist = static_cast<unsigned long long*>(work);
+  unsigned long long* clampc = hist + max_iters * g.J;
+  SolveCtl* ctl = reinterpret_cast<SolveCtl*>(clampc + max_iters);
+  cudaError_t e = cudaMemsetAsync(work, 0, static_cast<size_t>(solve_work_bytes(g, max_iters)), stream);
+  if (e != cudaSuccess) return e;
+  solve_init_kernel<<<1, 1, 0, stream>>>(ctl, max_iters);
+  count_launch();
+  e = refit(g, v, coef, stream);  // initial interpolants of buffer 0
+  if (e != cudaSuccess) return e;
+
+  SweepArgs a{};
+  a.g = g;
+  a.NP = NP;
+  a.nodes = nodes;
+  a.stacks = stacks;
+  a.stack_elems = stack_elems_of(g, NP);
+  a.hist_base = hist;
+  a.clamp_base = clampc;
+  a.ctl = ctl;
+  // graph body: two sweeps (buffer 0 -> 1 -> 0), each followed by its refit and stopping test
+  const int pairs = max_iters >= 256 ? 32 : static_cast<int>((max_iters + 1) / 2);
+  cudaStream_t cs;
+  e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return e;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  const long long launches0 = launch_count();
+  e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+  for (int r = 0; r < pairs && e == cudaSuccess; ++r) {
+    for (int half = 0; half < 2 && e == cudaSuccess; ++half) {
+      const long long src = half * JN, dst = (1 - half) * JN;
+      a.coef = coef + src;
+      a.v_old = v + src;
+      a.u_old = u + src;
+      a.v_new = v + dst;
+      a.u_new = u + dst;
+      e = launch_sweep(a, cs);
+      if (e == cudaSuccess) e = refit(g, v + dst, coef + dst, cs);
+      if (e == cudaSuccess) {
+        solve_finish_kernel<<<1, 1, 0, cs>>>(ctl, hist, g.J, g.tol);
+        e = cudaGetLastError();
+      }
+    }
+  }
+  cudaError_t e2 = cudaStreamEndCapture(cs, &graph);
+  if (e == cudaSuccess) e = e2;
+  const long long captured = launch_count() - launches0;  // counted once while capturing
+  const long long per_launch = captured + 2 * pairs;        // + the finish kernels
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
+  SolveCtl h{};
+  // the capture stream waits for the setup work on `stream`; results flow back the same way
+  cudaEvent_t ev = nullptr;
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(ev, stream);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev, 0);
+  long long launched = 0;
+  while (e == cudaSuccess) {
+    e = cudaGraphLaunch(exec, cs);
+    if (e != cudaSuccess) break;
+    launched += per_launch;
+    e = cudaMemcpyAsync(&h, ctl, sizeof(h), cudaMemcpyDeviceToHost, cs);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(cs);
+    if (e != cudaSuccess || h.done) break;
+  }
+  for (long long k = captured; k < launched; ++k) count_launch();  // graph replays run the same kernels
+  if (e == cudaSuccess) e = cudaEventRecord(ev, cs);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(stream, ev, 0);
+  if (ev) cudaEventDestroy(ev);
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
+  cudaStreamDestroy(cs);
+  if (e != cudaSuccess) return e;
+  *iterations = h.iterations;
+  *converged = h.converged;
+  *nonfinite = h.err ? 1 : 0;
+  return cudaSuccess;
+}
+
+cudaError_t maximise_rows(long long m, int L, const double* coef, const double* x0, double* x, double* f,
+                          int always_scan, cudaStream_t stream) {
+  if (m <= 0) return cudaSuccess;
+  const long long blocks = (m + kSweepWarps - 1) / kSweepWarps;
+  maximise_rows_kernel<<<static_cast<unsigned>(blocks), kSweepWarps * 32, 0, stream>>>(m, L, coef, x0, x, f,
+                                                                                       always_scan);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace cb
