@@ -16,8 +16,8 @@
 // compiled with -fmad=false; numpy's pairwise summation is reproduced), so on identical
 // coefficient rows it is bitwise identical to the reference (tested).
 //
-// The driver (`solve`, :495-570) captures [sweep -> refit (K1 transform) -> convergence test]
-// pairs in a CUDA graph; the sup-norm change per player is reduced with atomicMax on the IEEE bits
+// The driver (`solve`, :495-570) captures [sweep (+ convergence test by its last warp) -> refit
+// (K1 transform)] pairs in a CUDA graph; the sup-norm change per player is reduced with atomicMax on the IEEE bits
 // (non-negative doubles order like their bit patterns) and the stopping test runs on the device,
 // so the host only polls a flag once per graph launch.
 #include <cstdio>
@@ -45,7 +45,7 @@ struct SolveCtl {
   int done;
   int converged;
   unsigned err;          // non-finite objective seen
-  int pad;
+  unsigned arrived;      // warps of the running sweep that finished (last one runs the stopping test)
 };
 
 struct SweepArgs {
@@ -239,6 +239,28 @@ __device__ double eval_reversed(const double* C, int J, const int* np, const dou
   return acc[J - 1];
 }
 
+// stopping test of solve (:551-556): sup-norm change below tol -> converged.  Run by the last
+// warp of each sweep (after every warp's history update is visible).
+__device__ void solve_finish(SolveCtl* ctl, const unsigned long long* hist_base, int J, double tol) {
+  const long long it = ctl->it;
+  ctl->it = it + 1;
+  if (ctl->err) {
+    ctl->done = 1;
+    ctl->iterations = it + 1;
+    return;
+  }
+  double dmax = 0.0;
+  for (int i = 0; i < J; ++i) dmax = fmax(dmax, __longlong_as_double(static_cast<long long>(hist_base[it * J + i])));
+  if (dmax < tol) {
+    ctl->done = 1;
+    ctl->converged = 1;
+    ctl->iterations = it + 1;
+  } else if (it + 1 >= ctl->max_iters) {
+    ctl->done = 1;
+    ctl->iterations = it + 1;
+  }
+}
+
 __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(const __grid_constant__ SweepArgs a) {
   __shared__ double sT[kSweepWarps][kSolverMaxJ - 1][kKMax];   // bound players' basis rows
   __shared__ double sAcc[kSweepWarps][kKMax * kSolverMaxJ];      // drift polynomial (K, J)
@@ -287,32 +309,35 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(const __grid_co
     for (int l = 2; l < bsz[lane]; ++l) row[l] = x2 * row[l - 1] - row[l - 2];
   }
   __syncwarp();
-  // stack strides (C order over (nu_1, ..., nu_J), then the node axis)
-  long long stride[kSolverMaxJ];
+  // stack strides (C order over (nu_1, ..., nu_J)), in units of the node axis
+  int stride[kSolverMaxJ];
   {
-    long long s = 1;
+    int s = 1;
     for (int d = J - 1; d >= 0; --d) {
       stride[d] = s;
       s *= g.nu[d];
     }
   }
   // 2. bind: acc[l_own * J + comp] = sum over bound tuples of prod T * stack_comp[...]
+  //    (bound digits advance incrementally, last bound player fastest)
   for (int r = lane; r < K * J; r += 32) {
     const int lown = r / J, comp = r - (r / J) * J;
-    const double* S = a.stacks + static_cast<long long>(comp) * a.stack_elems;
+    const double* S = a.stacks + static_cast<long long>(comp) * a.stack_elems + p;
+    int tt[kSolverMaxJ - 1];
+    for (int t = 0; t < J - 1; ++t) tt[t] = 0;
+    int off = lown * stride[i];
     double acc = 0.0;
-    for (long long b = 0; b < NB; ++b) {
-      long long rem = b, off = static_cast<long long>(lown) * stride[i];
-      double w = 1.0;
-      int tt[kSolverMaxJ - 1];
-      for (int t = J - 2; t >= 0; --t) {
-        const long long q = rem / bsz[t];
-        tt[t] = static_cast<int>(rem - q * bsz[t]);
-        rem = q;
-        off += tt[t] * stride[bdim[t]];
+#pragma unroll 4
+    for (int b = 0; b < static_cast<int>(NB); ++b) {
+      double w = sT[warp][0][tt[0]];
+      for (int t = 1; t < J - 1; ++t) w = w * sT[warp][t][tt[t]];
+      acc = acc + w * __ldg(S + static_cast<long long>(off) * a.NP);
+      for (int t = J - 2; t >= 0; --t) {  // increment the bound digits
+        off += stride[bdim[t]];
+        if (++tt[t] < bsz[t]) break;
+        off -= bsz[t] * stride[bdim[t]];
+        tt[t] = 0;
       }
-      for (int t = 0; t < J - 1; ++t) w = (t == 0) ? sT[warp][0][tt[0]] : w * sT[warp][t][tt[t]];
-      acc = acc + w * S[off * a.NP + p];
     }
     sAcc[warp][r] = acc;
   }
@@ -390,6 +415,12 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(const __grid_co
     if (a.ctl) {
       const double d = fabs(fb - a.v_old[ip]);
       atomicMax(a.hist_base + it * J + i, static_cast<unsigned long long>(__double_as_longlong(d)));
+      __threadfence();
+      if (atomicAdd(&a.ctl->arrived, 1u) == static_cast<unsigned>(J * a.NP) - 1u) {
+        __threadfence();
+        a.ctl->arrived = 0;
+        solve_finish(a.ctl, a.hist_base, J, g.tol);
+      }
     }
   }
 }
@@ -401,28 +432,6 @@ __global__ void solve_init_kernel(SolveCtl* ctl, long long max_iters) {
   ctl->done = 0;
   ctl->converged = 0;
   ctl->err = 0;
-}
-
-// stopping test of solve (:551-556): sup-norm change below tol -> converged
-__global__ void solve_finish_kernel(SolveCtl* ctl, const unsigned long long* hist_base, int J, double tol) {
-  if (ctl->done) return;
-  const long long it = ctl->it;
-  ctl->it = it + 1;
-  if (ctl->err) {
-    ctl->done = 1;
-    ctl->iterations = it + 1;
-    return;
-  }
-  double dmax = 0.0;
-  for (int i = 0; i < J; ++i) dmax = fmax(dmax, __longlong_as_double(static_cast<long long>(hist_base[it * J + i])));
-  if (dmax < tol) {
-    ctl->done = 1;
-    ctl->converged = 1;
-    ctl->iterations = it + 1;
-  } else if (it + 1 >= ctl->max_iters) {
-    ctl->done = 1;
-    ctl->iterations = it + 1;
-  }
 }
 
 __global__ void maximise_rows_kernel(long long m, int L, const double* coef, const double* x0, double* x, double* f,
@@ -540,16 +549,12 @@ cudaError_t solve(const cb_game_t& g, const double* nodes, const double* stacks,
       a.u_new = u + dst;
       e = launch_sweep(a, cs);
       if (e == cudaSuccess) e = refit(g, v + dst, coef + dst, cs);
-      if (e == cudaSuccess) {
-        solve_finish_kernel<<<1, 1, 0, cs>>>(ctl, hist, g.J, g.tol);
-        e = cudaGetLastError();
-      }
     }
   }
   cudaError_t e2 = cudaStreamEndCapture(cs, &graph);
   if (e == cudaSuccess) e = e2;
   const long long captured = launch_count() - launches0;  // counted once while capturing
-  const long long per_launch = captured + 2 * pairs;        // + the finish kernels
+  const long long per_launch = captured;
   if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
   SolveCtl h{};
   // the capture stream waits for the setup work on `stream`; results flow back the same way
