@@ -228,6 +228,30 @@ def cpu_baseline(cfg: str, budget_s: float = 12.0):
             "sample": f"oracle build + {sample} of {N} advected nodes on {cores} threads, extrapolated to one step",
             "step_seconds": step_s,
         }
+    if cfg == "solve":
+        from oracle import solver_oracle as so
+
+        spec = solve_spec()
+        g = so.Game(J=spec.J, K=np.asarray(spec.K), beta=spec.beta, phi=spec.phi, A=spec.A, c=spec.c, m=spec.m,
+                    rho=spec.rho, h=spec.h, P_max=spec.P_max, U_max=spec.U_max, Np=spec.Np, Nu=spec.Nu,
+                    tol=spec.tol, max_iters=spec.max_iters)
+        S = so.Solver(g)
+        t0 = time.perf_counter()
+        S.solve(max_iters=20)
+        per = (time.perf_counter() - t0) / 20
+        n_s = int(max(20, min(5000, budget_s / max(per, 1e-9))))
+        t0 = time.perf_counter()
+        S.solve(max_iters=n_s)
+        per = (time.perf_counter() - t0) / n_s
+        return {
+            "value": 1.0 / per,
+            "unit": "sweeps/s",
+            "cores": 1,
+            "kind": "port",
+            "sample": f"oracle solver (numpy restatement of S/solver.py, one thread as the reference's "
+                      f"workers=1 default): first {n_s} sweeps of the same solve",
+            "step_seconds": per * SOLVE_SWEEPS,
+        }
     # 5a structured
     w = workloads.make("5a")
     t0 = time.perf_counter()
@@ -246,6 +270,15 @@ def cpu_baseline(cfg: str, budget_s: float = 12.0):
         "sample": "oracle build + eval_grid on a 5x25^5 slice of the 25^6 grid (numpy matmul, 1 BLAS thread), x5",
         "step_seconds": step_s,
     }
+
+
+SOLVE_SWEEPS = 66_755  # sweeps of the solve workload to convergence (measured; reported per run)
+
+
+def solve_spec():
+    import paper_2307_04688_b200 as cn
+
+    return cn.preset_spec("example1", tol=1e-8)
 
 
 def run_reference(args):
@@ -296,9 +329,13 @@ def workload_config(cfg: str, world: int):
                "M": 25 ** 6},
         "5b": {"workload": "config5b: J=6 n=13 advected-node time step (4,826,809 nodes)", "J": 6, "n": 13,
                "M": 13 ** 6},
+        "solve": {"workload": "solve: example1 preset (J=2, degree 8, h=1e-3) to tol=1e-8, the reference's "
+                              "acceptance fixture (T/test_acceptance.py:31-43); one step = one full solve",
+                  "J": 2, "n": 9, "M": 81},
     }[cfg]
     d = dict(desc)
-    d["parallelism"] = f"dp{world}" if cfg in ("1", "2", "4", "5a") else f"node-shard{world}+allgather"
+    d["parallelism"] = (f"dp{world}" if cfg in ("1", "2", "4", "5a") else
+                        "replicas" if cfg == "solve" else f"node-shard{world}+allgather")
     d["l2_flush"] = "256 MiB write between timed steps"
     return d
 
@@ -529,6 +566,50 @@ def run_ours(args):
         e2e = {"value": total_steps / e2e_s, "unit": "steps/s", "h2d_bytes_per_step": int(N * 8 / inner),
                "d2h_bytes_per_step": int(N * 8 / inner)}
         ms_per_step = 1000.0 * t_total / total_steps
+    elif cfg == "solve":
+        import warnings
+
+        spec = solve_spec()
+        for _ in range(args.warmup):
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore", RuntimeWarning)
+                cn.solve(cn.preset_spec("example1", tol=1e-8, max_iters=64))
+        torch.cuda.synchronize()
+        clocks = ClockSampler(local)
+        clocks.start()
+        launches0 = int(lib.cb_kernel_launches())
+        times, sweeps = [], []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore", RuntimeWarning)
+                res = cn.solve(spec)
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+            sweeps.append(res.iterations)
+        launches = int(lib.cb_kernel_launches()) - launches0
+        clk = clocks.stop()
+        t_total = max_over_ranks(sum(times), world, torch)
+        n_sw = sweeps[0]
+        value = world * sum(sweeps) / t_total
+        unit = "sweeps/s"
+        nodes = int(np.prod(spec.Np + 1))
+        K = int(spec.Nu[0]) + 1
+        evals = spec.J * nodes * K  # value-interpolant evaluations per sweep
+        flop_sweep = evals * 2 * sum(9 ** m for m in range(1, spec.J + 1))
+        achieved = flop_sweep * value / world / 1e12
+        roofline = {"bound": "fp64", "kernel": "sweep_kernel (warp per player x node; latency-bound)",
+                    "achieved": achieved, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+                    "frac": achieved / peaks["fp64_tflops"],
+                    "algorithmic": f"{flop_sweep} value-eval flops per sweep ({evals} evals)", "traffic": None}
+        e2e = {"value": value, "unit": unit, "h2d_bytes_per_step": int(8 * nodes * (spec.J + 2 * spec.J) +
+                                                                      8 * spec.J * nodes * K ** spec.J),
+               "d2h_bytes_per_step": int(8 * (3 * spec.J * nodes + n_sw * (spec.J + 1)))}
+        extra = {"sweeps_to_converge": n_sw, "solve_seconds": statistics.mean(times),
+                 "evals_per_s": value * evals, "converged": bool(res.converged)}
+        ms_per_step = 1000.0 * t_total / args.steps
     else:  # 5a structured
         w = workloads.make("5a")
         J, n = w.J, w.n
@@ -599,7 +680,7 @@ def run_ours(args):
             "warmup": args.warmup,
             "ms_per_step": ms_per_step,
             "higher_is_better": True,
-            "scaling": "weak" if cfg in ("1", "2", "4") else "strong",
+            "scaling": "weak" if cfg in ("1", "2", "4", "solve") else "strong",
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (seeded numpy, BASELINE.json shapes; no dataset)",
@@ -638,7 +719,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="2", choices=["1", "2", "3", "4", "5a", "5b"])
+    ap.add_argument("--config", default="2", choices=["1", "2", "3", "4", "5a", "5b", "solve"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU work per baseline sample")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")

@@ -181,6 +181,8 @@ def to_device(a):
         pinned = (not a.is_cuda) and a.is_pinned()
         return a.to(device=device(), dtype=t.float64, non_blocking=pinned).contiguous()
     arr = np.ascontiguousarray(np.asarray(a, dtype=float))
+    if not arr.flags.writeable:  # read-only views (frozen reference-style arrays): torch wants a copy
+        arr = arr.copy()
     host = t.from_numpy(arr)
     if arr.nbytes >= (1 << 20):
         host = host.pin_memory()
