@@ -199,6 +199,13 @@ int64_t cb_solve_work_bytes(const cb_game_t* game, int64_t max_iters);
 int cb_solve(const cb_game_t* game, const double* d_nodes, const double* d_stacks, double* d_v, double* d_u,
              double* d_coef, void* d_work, int64_t max_iters, int64_t* iterations, int* converged, void* stream);
 
+/* Closed-loop rollouts `simulate` (solver.py:597-629), batched over `batch` initial states:
+ * u_t = clip(policy(p_t), 0, U_max), p_{t+1} = clip(p_t + h g(p_t, u_t), 0, P_max) (game.py:165-168).
+ * d_policies: the J policy interpolants (fit_policy, solver.py:577-583), dense C-order
+ * (np_1..np_J) each, concatenated; d_p0 (batch, J); d_states, d_controls (batch, n_steps+1, J). */
+int cb_simulate(const cb_game_t* game, int64_t batch, const double* d_policies, const double* d_p0, int64_t n_steps,
+                double* d_states, double* d_controls, void* stream);
+
 /* Safeguarded maximiser _maximise_block (solver.py:262-323) on m rows of L coefficients
  * (reference variable on [-1, 1]) from warm starts d_x0: d_x, d_f (m,).  always_scan != 0 adds the
  * dense-scan candidate for every row (newton_maximize, solver.py:326-356). */

@@ -83,6 +83,7 @@ SIGNATURES = {
     "cb_solve_work_bytes": (_c_i64, [_gamep, _c_i64]),
     "cb_solve": (_c_int, [_gamep, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _i64p, ctypes.POINTER(_c_int), _vp]),
     "cb_maximise_rows": (_c_int, [_c_i64, _c_int, _vp, _vp, _vp, _vp, _c_int, _vp]),
+    "cb_simulate": (_c_int, [_gamep, _c_i64, _vp, _vp, _c_i64, _vp, _vp, _vp]),
 }
 
 _lib = None

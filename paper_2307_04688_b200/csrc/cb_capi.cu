@@ -512,3 +512,13 @@ int cb_maximise_rows(int64_t m, int L, const double* d_coef, const double* d_x0,
           "cb_maximise_rows");
   return CB_OK;
 }
+
+int cb_simulate(const cb_game_t* game, int64_t batch, const double* d_policies, const double* d_p0, int64_t n_steps,
+                double* d_states, double* d_controls, void* stream) {
+  int rc = check_game(game, "cb_simulate");
+  if (rc) return rc;
+  if (batch < 0 || n_steps < 0) return fail(CB_EINVAL, "cb_simulate: negative batch or step count");
+  CB_CUDA(simulate(*game, batch, d_policies, d_p0, n_steps, d_states, d_controls, static_cast<cudaStream_t>(stream)),
+          "cb_simulate");
+  return CB_OK;
+}

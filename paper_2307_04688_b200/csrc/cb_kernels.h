@@ -73,6 +73,8 @@ long long solve_work_bytes(const cb_game_t& g, long long max_iters);
 cudaError_t solve(const cb_game_t& g, const double* nodes, const double* stacks, double* v, double* u, double* coef,
                   void* work, long long max_iters, long long* iterations, int* converged, int* nonfinite,
                   cudaStream_t stream);
+cudaError_t simulate(const cb_game_t& g, long long B, const double* policies, const double* p0, long long n_steps,
+                     double* states, double* controls, cudaStream_t stream);
 cudaError_t maximise_rows(long long m, int L, const double* coef, const double* x0, double* x, double* f,
                           int always_scan, cudaStream_t stream);
 

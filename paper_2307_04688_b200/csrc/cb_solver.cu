@@ -452,6 +452,86 @@ __global__ void maximise_rows_kernel(long long m, int L, const double* coef, con
   }
 }
 
+
+// Closed-loop rollouts (simulate, S/solver.py:597-629): one warp per trajectory.  Per step the
+// lanes share the policy evaluation (flat coefficient index split across lanes, weights from
+// per-dim T tables in shared memory, warp-shuffle reduction), then lane 0 clips the controls,
+// records the row and takes the clipped Euler step of the drift (S/game.py:140-168).
+constexpr int kSimWarps = 4;
+constexpr int kSimMaxN = 64;
+
+__global__ void __launch_bounds__(kSimWarps * 32) simulate_kernel(const __grid_constant__ cb_game_t g, long long B,
+                                                                  const double* __restrict__ pol,
+                                                                  const double* __restrict__ p0, long long n_steps,
+                                                                  double* __restrict__ states,
+                                                                  double* __restrict__ controls) {
+  __shared__ double sT[kSimWarps][kSolverMaxJ][kSimMaxN];
+  __shared__ double sP[kSimWarps][kSolverMaxJ];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long b = static_cast<long long>(blockIdx.x) * kSimWarps + warp;
+  if (b >= B) return;
+  const int J = g.J;
+  long long N = 1;
+  for (int d = 0; d < J; ++d) N *= g.np[d];
+  const double scale = 2.0 / g.P_max;
+  double rowsum[kSolverMaxJ];
+  for (int i = 0; i < J; ++i) {
+    double s = 0.0;
+    for (int j = 0; j < J; ++j) s = s + g.K[i][j];
+    rowsum[i] = s;
+  }
+  if (lane < J) sP[warp][lane] = p0[b * J + lane];
+  __syncwarp();
+  for (long long t = 0; t <= n_steps; ++t) {
+    // basis tables T_l(scale * p_d - 1)
+    if (lane < J) {
+      const double x = scale * sP[warp][lane] - 1.0;
+      double* row = sT[warp][lane];
+      row[0] = 1.0;
+      if (g.np[lane] > 1) row[1] = x;
+      const double x2 = 2.0 * x;
+      for (int l = 2; l < g.np[lane]; ++l) row[l] = x2 * row[l - 1] - row[l - 2];
+    }
+    __syncwarp();
+    double u[kSolverMaxJ];
+    for (int i = 0; i < J; ++i) {
+      const double* C = pol + static_cast<long long>(i) * N;
+      double acc = 0.0;
+      for (long long e = lane; e < N; e += 32) {
+        long long rem = e;
+        double w = 1.0;
+        for (int d = J - 1; d >= 0; --d) {
+          const long long q = rem / g.np[d];
+          w = w * sT[warp][d][rem - q * g.np[d]];
+          rem = q;
+        }
+        acc = acc + w * C[e];
+      }
+      for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      u[i] = fmin(fmax(acc, 0.0), g.U_max);
+    }
+    if (lane == 0) {
+      double* srow = states + (b * (n_steps + 1) + t) * J;
+      double* crow = controls + (b * (n_steps + 1) + t) * J;
+      double p[kSolverMaxJ];
+      for (int d = 0; d < J; ++d) {
+        p[d] = sP[warp][d];
+        srow[d] = p[d];
+        crow[d] = u[d];
+      }
+      if (t < n_steps) {
+        for (int i = 0; i < J; ++i) {
+          double ex = 0.0;
+          for (int j = 0; j < J; ++j) ex = ex + p[j] * g.K[i][j];
+          const double gi = (ex - p[i] * rowsum[i]) / g.m[i] - g.c[i] * p[i] + g.beta[i] * u[i];
+          sP[warp][i] = fmin(fmax(p[i] + g.h * gi, 0.0), g.P_max);
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
 long long nodes_of(const cb_game_t& g) {
   long long n = 1;
   for (int d = 0; d < g.J; ++d) n *= g.np[d];
@@ -583,6 +663,16 @@ cudaError_t solve(const cb_game_t& g, const double* nodes, const double* stacks,
   *converged = h.converged;
   *nonfinite = h.err ? 1 : 0;
   return cudaSuccess;
+}
+
+cudaError_t simulate(const cb_game_t& g, long long B, const double* policies, const double* p0, long long n_steps,
+                     double* states, double* controls, cudaStream_t stream) {
+  if (B <= 0) return cudaSuccess;
+  const long long blocks = (B + kSimWarps - 1) / kSimWarps;
+  simulate_kernel<<<static_cast<unsigned>(blocks), kSimWarps * 32, 0, stream>>>(g, B, policies, p0, n_steps, states,
+                                                                               controls);
+  count_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t maximise_rows(long long m, int L, const double* coef, const double* x0, double* x, double* f,

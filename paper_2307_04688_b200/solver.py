@@ -30,6 +30,7 @@ _CLAMP_WARN_FRACTION = 0.01  # S/solver.py:54
 __all__ = [
     "BlockPlan", "partition", "ValueField", "PolicyField", "TimePath", "EquilibriumResult", "control_bases",
     "precompute_dynamics_stack", "newton_maximize", "bellman_sweep", "solve", "fit_policy", "simulate",
+    "simulate_batch",
 ]
 
 
@@ -358,10 +359,29 @@ def fit_policy(grid: StateGrid, policy: PolicyField) -> list[CoefTensor]:
             for i in range(policy.values.shape[0])]
 
 
-def simulate(spec: GameSpec, policies, p0, n_steps: int) -> TimePath:
-    """Closed-loop rollout u_n = clip(policy(p_n)), Euler step, repeat (S/solver.py:597-629)."""
-    from .chebnd import _eval_points_device
+def _simulate_device(spec: GameSpec, policies, P0: np.ndarray, n_steps: int):
+    J = spec.J
+    if len(policies) != J:
+        raise ValueError("need one policy interpolant per player")
+    grid = build_state_grid(spec)
+    for pol in policies:
+        if tuple(pol.shape) != grid.shape:
+            raise ValueError("policy interpolants and the state grid disagree on the shape")
+    t = _lib.require_cuda()
+    game = _game_struct(spec, grid)
+    pols = t.cat([pol.dense_device().reshape(-1) for pol in policies])
+    B = P0.shape[0]
+    dp0 = _lib.to_device(np.ascontiguousarray(P0, dtype=float))
+    states = _lib.empty((B, n_steps + 1, J))
+    controls = _lib.empty((B, n_steps + 1, J))
+    _lib.check(_lib.load().cb_simulate(ctypes.byref(game), B, _lib.ptr(pols), _lib.ptr(dp0), n_steps,
+                                       _lib.ptr(states), _lib.ptr(controls), _lib.stream_handle()), "simulate")
+    return _lib.to_host(states), _lib.to_host(controls)
 
+
+def simulate(spec: GameSpec, policies, p0, n_steps: int) -> TimePath:
+    """Closed-loop rollout u_n = clip(policy(p_n)), Euler step, repeat (S/solver.py:597-629); the
+    whole trajectory runs in one kernel (cb_simulate)."""
     J = spec.J
     if len(policies) != J:
         raise ValueError("need one policy interpolant per player")
@@ -369,16 +389,14 @@ def simulate(spec: GameSpec, policies, p0, n_steps: int) -> TimePath:
     if p.shape != (J,) or (p < 0.0).any() or (p > spec.P_max).any():
         raise ValueError(f"p0 must lie in [0, {spec.P_max}]^{J}")
     n_steps = int(n_steps)
-    states = np.empty((n_steps + 1, J))
-    controls = np.empty((n_steps + 1, J))
-    scale = 2.0 / spec.P_max
-    for k in range(n_steps + 1):
-        states[k] = p
-        x = _lib.to_device((scale * p - 1.0).reshape(1, J))
-        u = np.array([float(_lib.to_host(_eval_points_device(pol.shape, pol.device_coefficients, x))[0])
-                      for pol in policies])
-        u = np.clip(u, 0.0, spec.U_max)
-        controls[k] = u
-        if k < n_steps:
-            p = step(spec, p, u)
-    return TimePath(t=np.arange(n_steps + 1) * spec.h, states=states, controls=controls)
+    states, controls = _simulate_device(spec, policies, p.reshape(1, J), n_steps)
+    return TimePath(t=np.arange(n_steps + 1) * spec.h, states=states[0], controls=controls[0])
+
+
+def simulate_batch(spec: GameSpec, policies, p0s, n_steps: int) -> tuple[np.ndarray, np.ndarray]:
+    """Batched form of `simulate`: B initial states (B, J) -> states and controls
+    (B, n_steps + 1, J), one warp per trajectory."""
+    P0 = np.asarray(p0s, dtype=float)
+    if P0.ndim != 2 or P0.shape[1] != spec.J or (P0 < 0.0).any() or (P0 > spec.P_max).any():
+        raise ValueError(f"initial states must be (B, {spec.J}) inside [0, {spec.P_max}]")
+    return _simulate_device(spec, policies, P0, int(n_steps))

@@ -191,3 +191,43 @@ def test_nonfinite_initial_values_rejected(cuda):
         cn.solve(spec, init=(v, np.full((2, 9), 0.25)))
     with pytest.raises(ValueError):
         cn.solve(spec, init=(np.zeros((2, 9)), np.full((2, 9), 0.75)))
+
+
+def test_simulate_batch_matches_single(cuda):
+    spec = spec_of("e1b")
+    grid = cn.build_state_grid(spec)
+    pols = cn.fit_policy(grid, cn.PolicyField(GOLD["e1b_solve_policy"]))
+    P0 = np.array([[0.05, 0.3], [0.0, 0.0], [0.5, 0.5], [0.2, 0.1]])
+    S, U = cn.simulate_batch(spec, pols, P0, 300)
+    for b in range(P0.shape[0]):
+        path = cn.simulate(spec, pols, P0[b], 300)
+        assert np.array_equal(path.states, S[b]) and np.array_equal(path.controls, U[b])
+    with pytest.raises(ValueError):
+        cn.simulate(spec, pols, [0.6, 0.1], 10)
+    with pytest.raises(ValueError):
+        cn.simulate(spec, pols[:1], [0.1, 0.1], 10)
+
+
+def test_acceptance_value_consistency_and_symmetry(cuda):
+    """T/test_acceptance.py #9 (converged example1 values match truncated simulated payoffs from 10
+    nodes, horizon log(1e-8)/log(delta)) and #7 (player-exchange symmetries of the simulated
+    controls for example3 / example4), with the rollouts batched in one kernel."""
+    spec = cn.preset_spec("example1", tol=1e-8)
+    res = quiet(cn.solve, spec)
+    assert res.converged
+    grid = cn.build_state_grid(spec)
+    pols = cn.fit_policy(grid, res.policy)
+    horizon = int(np.ceil(np.log(1e-8) / np.log(spec.delta)))
+    nodes = np.random.default_rng(20240801 + 4).choice(grid.n_nodes, size=10, replace=False)
+    S, U = cn.simulate_batch(spec, pols, grid.nodes[nodes], horizon)
+    worst = 0.0
+    for k, j in enumerate(nodes):
+        pay = cn.discounted_payoff(spec, S[k], U[k], horizon)
+        worst = max(worst, float(np.max(np.abs(pay - res.values.values[:, j]))))
+    assert worst < max(1e-3, 10 * spec.tol)
+    for preset, (i, j) in {"example3": (0, 2), "example4": (2, 3)}.items():
+        sp = cn.preset_spec(preset)
+        r = quiet(cn.solve, sp)
+        assert r.converged
+        path = cn.simulate(sp, cn.fit_policy(cn.build_state_grid(sp), r.policy), np.zeros(sp.J), 10_000)
+        np.testing.assert_allclose(path.controls[:, i], path.controls[:, j], atol=1e-6)
