@@ -3,7 +3,7 @@
 # ncu launch list of the default bench command.  Usage: bash tools/bench_all.sh r01c
 tag=${1:-rXX}
 mkdir -p gpurun_out/$tag
-for c in 1 2 3 4 5a 5b; do
+for c in 1 2 3 4 5a 5b solve; do
   timeout 900 python bench.py --config $c > gpurun_out/$tag/bench_cfg$c.json 2> gpurun_out/$tag/bench_cfg$c.err
   echo "cfg $c rc=$?"; tail -c 400 gpurun_out/$tag/bench_cfg$c.json
 done
