@@ -173,17 +173,23 @@ typedef struct {
   double rnodes[CB_MAX_PLAYERS][CB_MAX_CONTROL_NODES]; /* reference_nodes(Nu_i) */
 } cb_game_t;
 
+/* Node-major drift tensors D_i[p][b][l_own][comp] (the reference's _PlayerWork.coeffs,
+ * solver.py:183-189) from the J control-space drift stacks (precompute_dynamics_stack,
+ * solver.py:141-159: each (nu_1, ..., nu_J, N_P) C-order, concatenated).  Done once per game;
+ * d_drift holds cb_solver_drift_elems() doubles. */
+int64_t cb_solver_drift_elems(const cb_game_t* game);
+int cb_solver_drift_layout(const cb_game_t* game, const double* d_stacks, double* d_drift, void* stream);
+
 /* One synchronous best-response sweep over all players and nodes: _run_sweep + _best_response_block
  * (solver.py:359-438), one warp per (player, node).
- *   d_nodes  (N_P, J) state nodes;  d_stacks: J drift stacks (precompute_dynamics_stack,
- *            solver.py:141-159), each (nu_1, ..., nu_J, N_P) C-order, concatenated;
+ *   d_nodes  (N_P, J) state nodes;  d_drift: cb_solver_drift_layout() of the drift stacks;
  *   d_coef   (J, N_P) value coefficients of the current fields, player i's tensor stored with
  *            REVERSED axes (l_J, ..., l_1) — exactly cb_transform_axes over axes 1..J of the node
  *            values viewed as (J, np_J, ..., np_1), i.e. _refit (solver.py:441-449) without a copy;
  *   d_v, d_u (J, N_P) current values / policy -> d_v_out, d_u_out (J, N_P);
  *   d_clamped: uint64 counter, incremented by the number of clamped successor components.
  * A non-finite objective sets d_status->nonfinite (FloatingPointError, solver.py:400-401). */
-int cb_bellman_sweep(const cb_game_t* game, const double* d_nodes, const double* d_stacks, const double* d_coef,
+int cb_bellman_sweep(const cb_game_t* game, const double* d_nodes, const double* d_drift, const double* d_coef,
                      const double* d_v, const double* d_u, double* d_v_out, double* d_u_out, uint64_t* d_clamped,
                      void* d_status, void* stream);
 
@@ -196,7 +202,7 @@ int64_t cb_solve_work_bytes(const cb_game_t* game, int64_t max_iters);
  * the final fields are in buffer (*iterations % 2).  d_work layout (cb_solve_work_bytes):
  *   [max_iters * J doubles: per-sweep per-player sup change][max_iters uint64: clamp counts][ctl].
  * Returns CB_ENONFINITE if a sweep produced a non-finite objective (*iterations = that sweep). */
-int cb_solve(const cb_game_t* game, const double* d_nodes, const double* d_stacks, double* d_v, double* d_u,
+int cb_solve(const cb_game_t* game, const double* d_nodes, const double* d_drift, double* d_v, double* d_u,
              double* d_coef, void* d_work, int64_t max_iters, int64_t* iterations, int* converged, void* stream);
 
 /* Closed-loop rollouts `simulate` (solver.py:597-629), batched over `batch` initial states:

@@ -472,12 +472,24 @@ static int check_game(const cb_game_t* g, const char* fn) {
   return CB_OK;
 }
 
-int cb_bellman_sweep(const cb_game_t* game, const double* d_nodes, const double* d_stacks, const double* d_coef,
+int64_t cb_solver_drift_elems(const cb_game_t* game) {
+  if (check_game(game, "cb_solver_drift_elems")) return -1;
+  return drift_elems(*game);
+}
+
+int cb_solver_drift_layout(const cb_game_t* game, const double* d_stacks, double* d_drift, void* stream) {
+  int rc = check_game(game, "cb_solver_drift_layout");
+  if (rc) return rc;
+  CB_CUDA(drift_layout(*game, d_stacks, d_drift, static_cast<cudaStream_t>(stream)), "cb_solver_drift_layout");
+  return CB_OK;
+}
+
+int cb_bellman_sweep(const cb_game_t* game, const double* d_nodes, const double* d_drift, const double* d_coef,
                      const double* d_v, const double* d_u, double* d_v_out, double* d_u_out, uint64_t* d_clamped,
                      void* d_status, void* stream) {
   int rc = check_game(game, "cb_bellman_sweep");
   if (rc) return rc;
-  CB_CUDA(bellman_sweep(*game, d_nodes, d_stacks, d_coef, d_v, d_u, d_v_out, d_u_out,
+  CB_CUDA(bellman_sweep(*game, d_nodes, d_drift, d_coef, d_v, d_u, d_v_out, d_u_out,
                         reinterpret_cast<unsigned long long*>(d_clamped), static_cast<Status*>(d_status),
                         static_cast<cudaStream_t>(stream)),
           "cb_bellman_sweep");
@@ -489,14 +501,14 @@ int64_t cb_solve_work_bytes(const cb_game_t* game, int64_t max_iters) {
   return solve_work_bytes(*game, max_iters);
 }
 
-int cb_solve(const cb_game_t* game, const double* d_nodes, const double* d_stacks, double* d_v, double* d_u,
+int cb_solve(const cb_game_t* game, const double* d_nodes, const double* d_drift, double* d_v, double* d_u,
              double* d_coef, void* d_work, int64_t max_iters, int64_t* iterations, int* converged, void* stream) {
   int rc = check_game(game, "cb_solve");
   if (rc) return rc;
   if (max_iters < 1) return fail(CB_EINVAL, "max_iters must be positive");
   long long its = 0;
   int conv = 0, nonfinite = 0;
-  CB_CUDA(solve(*game, d_nodes, d_stacks, d_v, d_u, d_coef, d_work, max_iters, &its, &conv, &nonfinite,
+  CB_CUDA(solve(*game, d_nodes, d_drift, d_v, d_u, d_coef, d_work, max_iters, &its, &conv, &nonfinite,
                 static_cast<cudaStream_t>(stream)),
           "cb_solve");
   *iterations = its;

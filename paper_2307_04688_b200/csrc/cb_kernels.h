@@ -66,11 +66,13 @@ cudaError_t eval_grid(const EvalLayout& L, const double* coef, const long long* 
 long long eval_grid_work_elems(const EvalLayout& L, const long long* k);
 
 // Collocation solver (cb_solver.cu).
-cudaError_t bellman_sweep(const cb_game_t& g, const double* nodes, const double* stacks, const double* coef,
+long long drift_elems(const cb_game_t& g);
+cudaError_t drift_layout(const cb_game_t& g, const double* stacks, double* drift, cudaStream_t stream);
+cudaError_t bellman_sweep(const cb_game_t& g, const double* nodes, const double* drift, const double* coef,
                           const double* v, const double* u, double* v_out, double* u_out,
                           unsigned long long* clamped, Status* st, cudaStream_t stream);
 long long solve_work_bytes(const cb_game_t& g, long long max_iters);
-cudaError_t solve(const cb_game_t& g, const double* nodes, const double* stacks, double* v, double* u, double* coef,
+cudaError_t solve(const cb_game_t& g, const double* nodes, const double* drift, double* v, double* u, double* coef,
                   void* work, long long max_iters, long long* iterations, int* converged, int* nonfinite,
                   cudaStream_t stream);
 cudaError_t simulate(const cb_game_t& g, long long B, const double* policies, const double* p0, long long n_steps,

@@ -33,6 +33,7 @@ namespace {
 constexpr int kSweepWarps = 4;
 constexpr int kSolverMaxJ = CB_MAX_PLAYERS;
 constexpr int kKMax = CB_MAX_CONTROL_NODES;
+constexpr int kSolverMaxN = 64;  // state nodes per dimension
 constexpr int kScanPoints = 257;   // S/solver.py:52
 constexpr int kBisect = 60;        // :53
 constexpr int kNewtonIter = 30;    // :50
@@ -52,8 +53,8 @@ struct SweepArgs {
   cb_game_t g;
   long long NP;
   const double* nodes;
-  const double* stacks;
-  long long stack_elems;  // prod(nu) * NP per stack
+  const double* drift;             // node-major drift tensors (cb_solver_drift_layout)
+  long long dofs[kSolverMaxJ];     // per-player offsets into `drift`
   const double* coef;
   const double* v_old;
   const double* u_old;
@@ -203,40 +204,59 @@ __device__ void warp_maximise(const double* c, int L, double x0, bool always_sca
 }
 
 // Value interpolant of one player at a point: coefficients with reversed axes (l_J, ..., l_1),
-// i.e. dim 0 is the memory-fastest axis; nested accumulation, dim 0 innermost.
+// i.e. dim 0 is the memory-fastest axis; nested accumulation, dim 0 innermost (the reference's
+// binding order).  The innermost row runs in scalar registers; the outer levels (fixed-size arrays
+// indexed by unrolled constants, so they stay in registers) are touched once per row.
 __device__ double eval_reversed(const double* C, int J, const int* np, const double* pt) {
   double x2[kSolverMaxJ], t[kSolverMaxJ], tp[kSolverMaxJ], acc[kSolverMaxJ];
-  int dig[kSolverMaxJ];
-  long long total = 1;
-  for (int d = 0; d < J; ++d) {
-    x2[d] = 2.0 * pt[d];
+  int dig[kSolverMaxJ], nn[kSolverMaxJ];
+  long long rows = 1;
+#pragma unroll
+  for (int d = 0; d < kSolverMaxJ; ++d) {
+    const bool on = d < J;
+    x2[d] = on ? 2.0 * pt[d] : 0.0;
     t[d] = 1.0;
-    tp[d] = pt[d];  // T_{-1} := x so that T_1 = 2x*T_0 - T_{-1} = x
+    tp[d] = on ? pt[d] : 0.0;  // T_{-1} := x so that T_1 = 2x*T_0 - T_{-1} = x
     acc[d] = 0.0;
     dig[d] = 0;
-    total *= np[d];
+    nn[d] = on ? np[d] : 1;
+    if (on && d > 0) rows *= np[d];
   }
-  for (long long e = 0; e < total; ++e) {
-    acc[0] = acc[0] + C[e] * t[0];
-    const double tn = x2[0] * t[0] - tp[0];
-    tp[0] = t[0];
-    t[0] = tn;
-    if (++dig[0] == np[0]) {
-      for (int L = 0; L + 1 < J; ++L) {
-        if (dig[L] != np[L]) break;
-        dig[L] = 0;
-        t[L] = 1.0;
-        tp[L] = 0.5 * x2[L];
-        acc[L + 1] = acc[L + 1] + acc[L] * t[L + 1];
-        acc[L] = 0.0;
-        const double tn2 = x2[L + 1] * t[L + 1] - tp[L + 1];
-        tp[L + 1] = t[L + 1];
-        t[L + 1] = tn2;
-        ++dig[L + 1];
+  const int n0 = nn[0];
+  const double xx2 = x2[0], x0 = 0.5 * x2[0];
+  double result = 0.0;
+  for (long long row = 0; row < rows; ++row, C += n0) {
+    double a0 = 0.0, t0 = 1.0, tp0 = x0;
+    for (int l = 0; l < n0; ++l) {
+      a0 = a0 + C[l] * t0;
+      const double tn = xx2 * t0 - tp0;
+      tp0 = t0;
+      t0 = tn;
+    }
+    double v = a0;
+    bool carry = true;
+#pragma unroll
+    for (int L = 1; L < kSolverMaxJ; ++L) {
+      if (carry && L < J) {
+        acc[L] = acc[L] + v * t[L];
+        const double tn = x2[L] * t[L] - tp[L];
+        tp[L] = t[L];
+        t[L] = tn;
+        if (++dig[L] < nn[L]) {
+          carry = false;
+        } else {
+          v = acc[L];
+          acc[L] = 0.0;
+          dig[L] = 0;
+          t[L] = 1.0;
+          tp[L] = 0.5 * x2[L];
+          if (L == J - 1) result = v;
+        }
       }
     }
+    if (J == 1) result = v;
   }
-  return acc[J - 1];
+  return result;
 }
 
 // stopping test of solve (:551-556): sup-norm change below tol -> converged.  Run by the last
@@ -268,6 +288,8 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(const __grid_co
   __shared__ double sCoef[kSweepWarps][kKMax];
   __shared__ double sQ1[kSweepWarps][kKMax];
   __shared__ double sQ2[kSweepWarps][kKMax];
+  __shared__ double sPt[kSweepWarps][kKMax][kSolverMaxJ];        // successor points (reference coords)
+  __shared__ double sTv[kSweepWarps][kSolverMaxJ][kSolverMaxN];  // value basis rows of one successor
   const cb_game_t& g = a.g;
   const int J = g.J;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -309,37 +331,27 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(const __grid_co
     for (int l = 2; l < bsz[lane]; ++l) row[l] = x2 * row[l - 1] - row[l - 2];
   }
   __syncwarp();
-  // stack strides (C order over (nu_1, ..., nu_J)), in units of the node axis
-  int stride[kSolverMaxJ];
+  // 2. bind: acc[l_own * J + comp] = sum over bound tuples b of prod T * D_i[p][b][l_own][comp];
+  //    the node-major layout makes each b a contiguous (K, J) block: coalesced lane reads
   {
-    int s = 1;
-    for (int d = J - 1; d >= 0; --d) {
-      stride[d] = s;
-      s *= g.nu[d];
-    }
-  }
-  // 2. bind: acc[l_own * J + comp] = sum over bound tuples of prod T * stack_comp[...]
-  //    (bound digits advance incrementally, last bound player fastest)
-  for (int r = lane; r < K * J; r += 32) {
-    const int lown = r / J, comp = r - (r / J) * J;
-    const double* S = a.stacks + static_cast<long long>(comp) * a.stack_elems + p;
-    int tt[kSolverMaxJ - 1];
-    for (int t = 0; t < J - 1; ++t) tt[t] = 0;
-    int off = lown * stride[i];
-    double acc = 0.0;
-#pragma unroll 4
-    for (int b = 0; b < static_cast<int>(NB); ++b) {
-      double w = sT[warp][0][tt[0]];
-      for (int t = 1; t < J - 1; ++t) w = w * sT[warp][t][tt[t]];
-      acc = acc + w * __ldg(S + static_cast<long long>(off) * a.NP);
-      for (int t = J - 2; t >= 0; --t) {  // increment the bound digits
-        off += stride[bdim[t]];
-        if (++tt[t] < bsz[t]) break;
-        off -= bsz[t] * stride[bdim[t]];
-        tt[t] = 0;
+    const int KJ = K * J;
+    const double* D = a.drift + a.dofs[i] + static_cast<long long>(p) * NB * KJ;
+    for (int r = lane; r < KJ; r += 32) {
+      int tt[kSolverMaxJ - 1];
+      for (int t = 0; t < J - 1; ++t) tt[t] = 0;
+      double acc = 0.0;
+#pragma unroll 8
+      for (int b = 0; b < static_cast<int>(NB); ++b) {
+        double w = sT[warp][0][tt[0]];
+        for (int t = 1; t < J - 1; ++t) w = w * sT[warp][t][tt[t]];
+        acc = acc + w * __ldg(D + static_cast<long long>(b) * KJ + r);
+        for (int t = J - 2; t >= 0; --t) {  // next bound tuple (last bound player fastest)
+          if (++tt[t] < bsz[t]) break;
+          tt[t] = 0;
+        }
       }
+      sAcc[warp][r] = acc;
     }
-    sAcc[warp][r] = acc;
   }
   __syncwarp();
   // 3. own-control node k = lane: drift, successor, value, objective
@@ -365,7 +377,61 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(const __grid_co
       clamped += (cl != nxt) ? 1u : 0u;
       pt[c] = cl * p_scale - 1.0;
     }
-    const double vnext = eval_reversed(a.coef + static_cast<long long>(i) * a.NP, J, g.np, pt);
+    for (int c = 0; c < J; ++c) sPt[warp][k][c] = pt[c];
+  }
+  __syncwarp();
+  // value interpolant at the K successors: one lane per point for small tensors; the whole warp
+  // per point (flat coefficient index split over lanes, T tables in smem, shuffle reduction) when
+  // the tensor has more than 128 coefficients
+  double vnext = 0.0;
+  const double* Ci = a.coef + static_cast<long long>(i) * a.NP;
+  if (a.NP <= 128) {
+    if (lane < K) vnext = eval_reversed(Ci, J, g.np, sPt[warp][lane]);
+  } else {
+    int d0[kSolverMaxJ], d32[kSolverMaxJ];
+    {
+      int r0 = lane, r32 = 32;
+      for (int d = 0; d < J; ++d) {
+        d0[d] = r0 % g.np[d];
+        r0 /= g.np[d];
+        d32[d] = r32 % g.np[d];
+        r32 /= g.np[d];
+      }
+    }
+    for (int k = 0; k < K; ++k) {
+      if (lane < J) {
+        const double x = sPt[warp][k][lane];
+        double* row = sTv[warp][lane];
+        row[0] = 1.0;
+        if (g.np[lane] > 1) row[1] = x;
+        const double x2 = 2.0 * x;
+        for (int l = 2; l < g.np[lane]; ++l) row[l] = x2 * row[l - 1] - row[l - 2];
+      }
+      __syncwarp();
+      int dg[kSolverMaxJ];
+      for (int d = 0; d < J; ++d) dg[d] = d0[d];
+      double part = 0.0;
+      for (long long e = lane; e < a.NP; e += 32) {
+        double w = sTv[warp][0][dg[0]];
+        for (int d = 1; d < J; ++d) w = w * sTv[warp][d][dg[d]];
+        part = part + w * __ldg(Ci + e);
+        int carry = 0;  // flat index += 32 in the mixed radix of the tensor
+        for (int d = 0; d < J; ++d) {
+          dg[d] += d32[d] + carry;
+          carry = 0;
+          while (dg[d] >= g.np[d]) {
+            dg[d] -= g.np[d];
+            ++carry;
+          }
+        }
+      }
+      for (int o = 16; o >= 1; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if (lane == k) vnext = part;
+      __syncwarp();
+    }
+  }
+  if (lane < K) {
+    const int k = lane;
     const double un = g.unodes[i][k];
     const double gain = un * (g.A[i] - 0.5 * un);
     const double xi = a.nodes[p * J + i];
@@ -532,16 +598,57 @@ __global__ void __launch_bounds__(kSimWarps * 32) simulate_kernel(const __grid_c
   }
 }
 
+
+// Node-major drift tensors D_i[p][b][l_own][comp] (the reference's _PlayerWork.coeffs layout,
+// S/solver.py:183-189) from the J control-space stacks (nu_1..nu_J, N_P): one thread per element.
+__global__ void drift_layout_kernel(const __grid_constant__ cb_game_t g, long long NP, const double* __restrict__ stacks,
+                                    double* __restrict__ drift, int i, long long total) {
+  const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  const int J = g.J, K = g.nu[i];
+  long long rem = e;
+  const int comp = static_cast<int>(rem % J);
+  rem /= J;
+  const int lown = static_cast<int>(rem % K);
+  rem /= K;
+  long long NB = 1;
+  for (int j = 0; j < J; ++j)
+    if (j != i) NB *= g.nu[j];
+  long long b = rem % NB;
+  const long long p = rem / NB;
+  int l[kSolverMaxJ];
+  l[i] = lown;
+  for (int j = J - 1; j >= 0; --j) {
+    if (j == i) continue;
+    l[j] = static_cast<int>(b % g.nu[j]);
+    b /= g.nu[j];
+  }
+  long long off = 0, selems = NP;
+  for (int j = 0; j < J; ++j) {
+    off = off * g.nu[j] + l[j];
+    selems *= g.nu[j];
+  }
+  drift[e] = stacks[comp * selems + off * NP + p];
+}
+
 long long nodes_of(const cb_game_t& g) {
   long long n = 1;
   for (int d = 0; d < g.J; ++d) n *= g.np[d];
   return n;
 }
 
-long long stack_elems_of(const cb_game_t& g, long long NP) {
-  long long s = NP;
-  for (int d = 0; d < g.J; ++d) s *= g.nu[d];
-  return s;
+// per-player element counts / offsets of the node-major drift tensors
+long long drift_offsets(const cb_game_t& g, long long* dofs) {
+  const long long NP = nodes_of(g);
+  long long total = 0;
+  for (int i = 0; i < g.J; ++i) {
+    long long NB = 1;
+    for (int j = 0; j < g.J; ++j)
+      if (j != i) NB *= g.nu[j];
+    if (dofs) dofs[i] = total;
+    total += NP * NB * g.nu[i] * g.J;
+  }
+  return total;
 }
 
 cudaError_t launch_sweep(const SweepArgs& a, cudaStream_t s) {
@@ -563,15 +670,15 @@ cudaError_t refit(const cb_game_t& g, const double* v, double* coef, cudaStream_
 
 }  // namespace
 
-cudaError_t bellman_sweep(const cb_game_t& g, const double* nodes, const double* stacks, const double* coef,
+cudaError_t bellman_sweep(const cb_game_t& g, const double* nodes, const double* drift, const double* coef,
                           const double* v, const double* u, double* v_out, double* u_out,
                           unsigned long long* clamped, Status* st, cudaStream_t stream) {
   SweepArgs a{};
   a.g = g;
   a.NP = nodes_of(g);
   a.nodes = nodes;
-  a.stacks = stacks;
-  a.stack_elems = stack_elems_of(g, a.NP);
+  a.drift = drift;
+  drift_offsets(g, a.dofs);
   a.coef = coef;
   a.v_old = v;
   a.u_old = u;
@@ -582,11 +689,31 @@ cudaError_t bellman_sweep(const cb_game_t& g, const double* nodes, const double*
   return launch_sweep(a, stream);
 }
 
+long long drift_elems(const cb_game_t& g) { return drift_offsets(g, nullptr); }
+
+cudaError_t drift_layout(const cb_game_t& g, const double* stacks, double* drift, cudaStream_t stream) {
+  const long long NP = nodes_of(g);
+  long long dofs[kSolverMaxJ];
+  drift_offsets(g, dofs);
+  for (int i = 0; i < g.J; ++i) {
+    long long NB = 1;
+    for (int j = 0; j < g.J; ++j)
+      if (j != i) NB *= g.nu[j];
+    const long long total = NP * NB * g.nu[i] * g.J;
+    drift_layout_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, stream>>>(g, NP, stacks, drift + dofs[i],
+                                                                                      i, total);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 long long solve_work_bytes(const cb_game_t& g, long long max_iters) {
   return max_iters * g.J * 8 + max_iters * 8 + 64;
 }
 
-cudaError_t solve(const cb_game_t& g, const double* nodes, const double* stacks, double* v, double* u, double* coef,
+cudaError_t solve(const cb_game_t& g, const double* nodes, const double* drift, double* v, double* u, double* coef,
                   void* work, long long max_iters, long long* iterations, int* converged, int* nonfinite,
                   cudaStream_t stream) {
   const long long NP = nodes_of(g);
@@ -605,8 +732,8 @@ cudaError_t solve(const cb_game_t& g, const double* nodes, const double* stacks,
   a.g = g;
   a.NP = NP;
   a.nodes = nodes;
-  a.stacks = stacks;
-  a.stack_elems = stack_elems_of(g, NP);
+  a.drift = drift;
+  drift_offsets(g, a.dofs);
   a.hist_base = hist;
   a.clamp_base = clampc;
   a.ctl = ctl;

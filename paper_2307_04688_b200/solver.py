@@ -171,7 +171,12 @@ class _Device:
         self.game = _game_struct(spec, grid)
         self.n = grid.n_nodes
         self.nodes = _lib.to_device(np.ascontiguousarray(grid.nodes))
-        self.stacks = t.cat([_lib.to_device(st.device_coefficients).reshape(-1) for st in stacks])
+        stk = t.cat([_lib.to_device(st.device_coefficients).reshape(-1) for st in stacks])
+        lib = _lib.load()
+        # node-major per-player drift tensors (the reference's _PlayerWork.coeffs), built once
+        self.drift = _lib.empty((int(lib.cb_solver_drift_elems(ctypes.byref(self.game))),))
+        _lib.check(lib.cb_solver_drift_layout(ctypes.byref(self.game), _lib.ptr(stk), _lib.ptr(self.drift),
+                                              _lib.stream_handle()), "drift layout")
         # node values (J, N_P) read as (J, np_J, ..., np_1): the refit transform gives reversed-axis
         # coefficient tensors (no order="F" copy, S/solver.py:446)
         self.rev_shape = (spec.J,) + tuple(reversed(grid.shape))
@@ -263,7 +268,7 @@ def bellman_sweep(spec: GameSpec, grid: StateGrid, values: ValueField, policy: P
     u_out = _lib.empty((J, n))
     clamped = t.zeros(1, dtype=t.int64, device=_lib.device())
     st = _lib.new_status()
-    _lib.check(_lib.load().cb_bellman_sweep(ctypes.byref(dev.game), _lib.ptr(dev.nodes), _lib.ptr(dev.stacks),
+    _lib.check(_lib.load().cb_bellman_sweep(ctypes.byref(dev.game), _lib.ptr(dev.nodes), _lib.ptr(dev.drift),
                                             _lib.ptr(coef), _lib.ptr(v), _lib.ptr(u), _lib.ptr(v_out),
                                             _lib.ptr(u_out), _lib.ptr(clamped), _lib.ptr(st), _lib.stream_handle()),
                "bellman_sweep")
@@ -325,7 +330,7 @@ def solve(spec: GameSpec, plan: BlockPlan | None = None, init=None, workers: int
     t_setup = time.perf_counter() - t_start
     iters = ctypes.c_int64(0)
     conv = ctypes.c_int(0)
-    rc = lib.cb_solve(ctypes.byref(dev.game), _lib.ptr(dev.nodes), _lib.ptr(dev.stacks), _lib.ptr(v), _lib.ptr(u),
+    rc = lib.cb_solve(ctypes.byref(dev.game), _lib.ptr(dev.nodes), _lib.ptr(dev.drift), _lib.ptr(v), _lib.ptr(u),
                       _lib.ptr(coef), _lib.ptr(work), max_iters, ctypes.byref(iters), ctypes.byref(conv),
                       _lib.stream_handle())
     _lib.check(rc, "solve")
