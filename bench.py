@@ -623,10 +623,19 @@ def run_ours(args):
         targets = [w.targets[0][a:b]] + list(w.targets[1:])
         vals_dev = _lib.to_device(w.values)
         tdev = [_lib.to_device(t) for t in targets]
+        from paper_2307_04688_b200.chebnd import _eval_grid_device
+
+        L = _lib.eval_layout(shape)
+        coef5 = _lib.empty((L["elems"],))
+        st5 = _lib.new_status()
+        grid_out = _lib.empty(tuple(int(t.shape[0]) for t in tdev))
+        grid_work = [None]
 
         def step():
-            t = cn.tensor_coeffs(vals_dev, bases)
-            return cn.eval_grid(t, tdev)
+            # device-resident build + structured evaluation (no host syncs; the public-API path
+            # with its status checks is the e2e leg below)
+            tensor_coeffs_device(vals_dev, shape, out=coef5, status=st5)
+            return _eval_grid_device(shape, coef5, tdev, status=st5, out=grid_out)
 
         for _ in range(args.warmup):
             step()

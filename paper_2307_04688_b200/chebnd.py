@@ -519,6 +519,30 @@ def eval_diagonal_batch(stack: TensorStack, points, gather: GatherIndex) -> Tens
     return TensorStack(tuple(stack.bases[1:]), out)
 
 
+def _eval_grid_device(shape, coef_dev, targets_dev, status=None, work=None, out=None):
+    """Device-resident structured evaluation without host synchronisation (K3): eval-layout
+    coefficients + per-dim CUDA target vectors -> CUDA (k_1, ..., k_J)."""
+    J = len(shape)
+    ks = [int(tv.shape[0]) for tv in targets_dev]
+    # all J evaluation matrices in one allocation (the C side reads them stream-ordered)
+    Eall = _lib.empty((sum(k * n for k, n in zip(ks, shape)),))
+    Es, off = [], 0
+    for j, tv in enumerate(targets_dev):
+        view = Eall[off:off + ks[j] * shape[j]].view(ks[j], shape[j])
+        Es.append(_basis_device(tv, shape[j], True, status, out=view))
+        off += ks[j] * shape[j]
+    lib = _lib.load()
+    work_elems = int(lib.cb_eval_grid_workspace(J, _lib.i64_array(shape), _lib.i64_array(ks)))
+    if work is None or work.numel() < max(1, work_elems):
+        work = _lib.empty((max(1, work_elems),))
+    if out is None:
+        out = _lib.empty(tuple(ks))
+    eptrs = (ctypes.c_void_p * J)(*[_lib.ptr(e) for e in Es])
+    _lib.check(lib.cb_eval_grid(J, _lib.i64_array(shape), _lib.ptr(coef_dev), _lib.i64_array(ks), eptrs,
+                                _lib.ptr(out), _lib.ptr(work), work_elems, _lib.stream_handle()), "eval_grid")
+    return out
+
+
 def eval_grid(tensor: CoefTensor, targets):
     """Structured evaluation on a tensor-product target grid: J successive eval_axis mode products
     (S/chebnd.py:209-233; the paper's pagemtimes evaluation P:385-417).  targets[j] are reference
@@ -526,29 +550,14 @@ def eval_grid(tensor: CoefTensor, targets):
     J = tensor.ndim
     if len(targets) != J:
         raise ValueError(f"need {J} target lists, got {len(targets)}")
-    shape = tensor.shape
     tvs = []
     for t in targets:
         tv = t if _is_tensor(t) else np.asarray(t, dtype=float)
         if tv.ndim != 1 or tv.shape[0] == 0:
             raise ValueError("points must be a non-empty one-dimensional list")
-        tvs.append(tv)
-    ks = [int(tv.shape[0]) for tv in tvs]
-    # all J evaluation matrices in one allocation (the C side fetches them with one copy)
-    Eall = _lib.empty((sum(k * n for k, n in zip(ks, shape)),))
-    Es, off = [], 0
+        tvs.append(_lib.to_device(tv))
     st = _lib.new_status()
-    for j, tv in enumerate(tvs):
-        view = Eall[off:off + ks[j] * shape[j]].view(ks[j], shape[j])
-        Es.append(_basis_device(_lib.to_device(tv), shape[j], True, st, out=view))
-        off += ks[j] * shape[j]
-    lib = _lib.load()
-    work_elems = int(lib.cb_eval_grid_workspace(J, _lib.i64_array(shape), _lib.i64_array(ks)))
-    work = _lib.empty((max(1, work_elems),))
-    out = _lib.empty(tuple(ks))
-    eptrs = (ctypes.c_void_p * J)(*[_lib.ptr(e) for e in Es])
-    _lib.check(lib.cb_eval_grid(J, _lib.i64_array(shape), _lib.ptr(tensor.device_coefficients), _lib.i64_array(ks),
-                                eptrs, _lib.ptr(out), _lib.ptr(work), work_elems, _lib.stream_handle()), "eval_grid")
+    out = _eval_grid_device(tensor.shape, tensor.device_coefficients, tvs, status=st)
     _lib.raise_for_points(st)
     return out if any(_is_tensor(t) for t in targets) else _lib.to_host(out)
 
