@@ -318,6 +318,7 @@ cudaError_t launch_pass(PassParams& p, cudaStream_t stream) {
 // rides in the kernel parameters and unrolled FMAs take it as constant-bank operands.
 // ------------------------------------------------------------------------------------------
 constexpr int kFiberThreads = 128;
+constexpr long long kFiberMinFibers = 1;  // fiber passes whenever every mode has n <= 34
 constexpr int kFMat = 34 * 18;
 
 struct FiberParams {
@@ -447,6 +448,19 @@ bool launch_fiber_pass(int nd, const long long* sizes, const long long* sin, con
   return true;
 }
 
+
+// Zero the pad columns [K, Kp) of rows [0, R) and the pad rows [R, R8) of an eval-layout tensor
+// (one launch instead of a 2-D memset with a 3-column width plus a row memset).
+__global__ void zero_pad_kernel(double* out, long long R, long long R8, long long K, long long Kp) {
+  const long long pc = Kp - K;
+  const long long n1 = R * pc, n2 = (R8 - R) * Kp;
+  for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < n1 + n2;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    if (e < n1) out[(e / pc) * Kp + K + (e % pc)] = 0.0;
+    else out[R * Kp + (e - n1)] = 0.0;
+  }
+}
+
 }  // namespace
 
 // Transform the consecutive axes [a0, a1) of a dense C-order array `shape` (ndim dims).
@@ -473,7 +487,7 @@ cudaError_t transform_axes(int ndim, const long long* shape, int a0, int a1, con
       const long long fb = total / shape[d];
       if (min_fibers < 0 || fb < min_fibers) min_fibers = fb;
     }
-    if (small_modes && min_fibers >= 2048 && ndim <= kMaxDims + 1) {
+    if (small_modes && min_fibers >= kFiberMinFibers && ndim <= kMaxDims + 1) {
       // strides: input dense C-order; output dense or the eval layout (leading rows x Kp pitch)
       long long sin[kMaxDims + 1], sout[kMaxDims + 1];
       long long acc = 1;
@@ -493,9 +507,13 @@ cudaError_t transform_axes(int ndim, const long long* shape, int a0, int a1, con
           a3 *= shape[d];
         }
         // zero the pad columns / rows (never written by the passes)
-        if (evl->Kp > evl->K) {
-          cudaError_t e = cudaMemset2DAsync(out + evl->K, sizeof(double) * evl->Kp, 0, sizeof(double) * (evl->Kp - evl->K),
-                                            evl->R, stream);
+        if (evl->Kp > evl->K || evl->R8 > evl->R) {
+          const long long n = evl->R * (evl->Kp - evl->K) + (evl->R8 - evl->R) * evl->Kp;
+          long long g = (n + 255) / 256;
+          if (g > num_sms() * 4LL) g = num_sms() * 4LL;
+          zero_pad_kernel<<<static_cast<unsigned>(g), 256, 0, stream>>>(out, evl->R, evl->R8, evl->K, evl->Kp);
+          count_launch();
+          cudaError_t e = cudaGetLastError();
           if (e != cudaSuccess) return e;
         }
       } else {
@@ -512,8 +530,6 @@ cudaError_t transform_axes(int ndim, const long long* shape, int a0, int a1, con
         cur = out;
         first = false;
       }
-      if (evl && evl->R8 > evl->R)
-        return cudaMemsetAsync(out + evl->R * evl->Kp, 0, sizeof(double) * (evl->R8 - evl->R) * evl->Kp, stream);
       return cudaSuccess;
     }
   }
