@@ -593,25 +593,41 @@ cudaError_t eval_grid(const EvalLayout& L, const double* coef, const long long* 
     if (err != cudaSuccess) return err;
     cur = bufA;
   }
-  const int single_passes = fuse ? J - 2 : J;
+  // pass plan, left to right: a pair of equal modes with an instantiated fused kernel goes in one
+  // fused pass (rotating layout in (n, n, R) -> out (R, k, k)), any other mode in a single
+  // rotating pass; the final pair is fused only when grid_fuse_last_two (padding carried, q = 2)
+  const bool padded = fuse && L.q == 2;  // modes J-2, J-1 travel as one padded Kp axis
+  auto pairable = [&](int d) {
+    if (d + 1 >= J || L.n[d] != L.n[d + 1] || k[d] != k[d + 1]) return false;
+    if (d + 2 == J) return fuse;
+    if (padded && d + 1 >= J - 2) return false;
+    return (L.n[d] == 13 && k[d] == 25) || (L.n[d] == 5 && k[d] == 4);
+  };
   auto const_ok = [&](int d) { return L.n[d] == 13 && k[d] == 25; };
   ConstSlotGuard guard(stream);
   if (guard.err != cudaSuccess) return guard.err;
-  for (int d = 0; d < single_passes; ++d) {
-    const long long R = total / L.n[d];
-    double* dst = (d == J - 1) ? out : ((cur == bufA) ? bufB : bufA);
-    cudaError_t err = const_ok(d) ? launch_rotate_const<13, 25>(E[d], cur, dst, R, stream)
-                                  : contract_axis(1, static_cast<int>(L.n[d]), R, 1, static_cast<int>(k[d]), E[d], cur,
-                                                  dst, 0, 1, k[d], stream);
+  int d = 0;
+  while (d < J) {
+    const bool pair = pairable(d);
+    const int last = pair ? d + 1 : d;
+    double* dst = (last == J - 1) ? out : ((cur == bufA) ? bufB : bufA);
+    cudaError_t err;
+    if (pair) {
+      const long long n = L.n[d], kk = k[d];
+      const long long R = total / ((last == J - 1 && L.q == 2) ? L.Kp : n * n);
+      if (n == 13 && kk == 25) err = launch_fused2<13, 25>(E[d], E[d + 1], cur, dst, R, stream);
+      else err = launch_fused2<5, 4>(E[d], E[d + 1], cur, dst, R, stream);
+      total = R * kk * kk;
+    } else {
+      const long long R = total / L.n[d];
+      err = const_ok(d) ? launch_rotate_const<13, 25>(E[d], cur, dst, R, stream)
+                        : contract_axis(1, static_cast<int>(L.n[d]), R, 1, static_cast<int>(k[d]), E[d], cur, dst, 0, 1,
+                                        k[d], stream);
+      total = R * k[d];
+    }
     if (err != cudaSuccess) return err;
-    total = R * k[d];
     cur = dst;
-  }
-  if (fuse) {
-    const long long n = L.n[J - 1], kk = k[J - 1];
-    const long long R = total / ((L.q == 2) ? L.Kp : n * n);
-    if (n == 13 && kk == 25) return launch_fused2<13, 25>(E[J - 2], E[J - 1], cur, out, R, stream);
-    if (n == 5 && kk == 4) return launch_fused2<5, 4>(E[J - 2], E[J - 1], cur, out, R, stream);
+    d = last + 1;
   }
   return cudaSuccess;
 }

@@ -289,7 +289,10 @@ def test_eval_1d_clenshaw_derivative(cuda):
                                      ((13, 13, 13, 13), (25, 25, 25, 25)), ((4, 17, 17), (3, 25, 25)),
                                      # fused last pair: q = 1 (unpadded copy) and q = 2 (padded rows carried)
                                      ((3, 5, 5), (2, 4, 4)), ((2, 13, 13), (3, 25, 25)), ((7, 3, 13, 13), (5, 4, 25, 25)),
-                                     ((40, 5, 5), (9, 4, 4))])
+                                     ((40, 5, 5), (9, 4, 4)),
+                                     # several fused pairs in sequence (config 5a's plan), odd J
+                                     ((5, 5, 5, 5, 3), (4, 4, 4, 4, 2)), ((13, 13, 5, 5, 5, 5), (25, 25, 4, 4, 4, 4)),
+                                     ((5, 5, 5, 5, 5), (4, 4, 4, 4, 4))])
 def test_eval_grid(cuda, shape, k):
     rng = np.random.default_rng(sum(shape))
     coef = rng.standard_normal(shape)
