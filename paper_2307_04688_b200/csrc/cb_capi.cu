@@ -202,7 +202,7 @@ int cb_eval_points(int J, const int64_t* n, const double* d_coef, int64_t M, con
 
 // Copy streams + events for the host-buffer pipeline (one set per device, created on first use).
 namespace {
-constexpr int kPipeMaxChunks = 8;
+constexpr int kPipeMaxChunks = 16;
 struct Pipe {
   cudaStream_t up = nullptr, down = nullptr;
   cudaEvent_t start = nullptr, done = nullptr;
@@ -245,17 +245,39 @@ int cb_eval_points_host(int J, const int64_t* n, const double* d_coef, int64_t M
   std::lock_guard<std::mutex> lock(g_pipe_mutex);
   Pipe* p = nullptr;
   CB_CUDA(pipe_for_device(&p), "cb_eval_points_host");
-  // chunks of >= 2^18 points (one evaluator launch stays several waves deep), at most 8
-  long long nch = M / (1LL << 18);
-  if (nch < 1) nch = 1;
-  if (nch > kPipeMaxChunks) nch = kPipeMaxChunks;
-  const long long per = (M + nch - 1) / nch;
+  // chunk plan: ramp up 2^15, 2^16, 2^17 and down 2^17, 2^16 (the first upload and the last
+  // download are the only exposed transfers), equal middle chunks of about 2^18 points (several
+  // evaluator waves each); at most 16 chunks
+  long long bounds[kPipeMaxChunks + 1];
+  int nch = 0;
+  {
+    long long sizes[kPipeMaxChunks];
+    long long rem = M;
+    int nh = 0, nt = 0;
+    long long head[3], tail[2];
+    for (long long s0 : {1LL << 15, 1LL << 16, 1LL << 17}) {
+      if (rem <= 0) break;
+      head[nh] = rem < s0 ? rem : s0;
+      rem -= head[nh++];
+    }
+    for (long long s0 : {1LL << 16, 1LL << 17}) {
+      if (rem <= (1LL << 18)) break;
+      tail[nt++] = s0;
+      rem -= s0;
+    }
+    long long nmid = rem > 0 ? (rem + (1LL << 18) - 1) >> 18 : 0;
+    if (nmid > kPipeMaxChunks - nh - nt) nmid = kPipeMaxChunks - nh - nt;
+    for (int i = 0; i < nh; ++i) sizes[nch++] = head[i];
+    for (long long i = 0; i < nmid; ++i) sizes[nch++] = rem / nmid + (i < rem % nmid ? 1 : 0);
+    for (int i = nt - 1; i >= 0; --i) sizes[nch++] = tail[i];
+    bounds[0] = 0;
+    for (int c = 0; c < nch; ++c) bounds[c + 1] = bounds[c] + sizes[c];
+  }
   CB_CUDA(cudaEventRecord(p->start, s), "cb_eval_points_host");  // inputs (coefficients) ready
   CB_CUDA(cudaStreamWaitEvent(p->up, p->start, 0), "cb_eval_points_host");
   CB_CUDA(cudaStreamWaitEvent(p->down, p->start, 0), "cb_eval_points_host");
-  for (long long c = 0; c < nch; ++c) {
-    const long long b = c * per, m = (b + per <= M) ? per : M - b;
-    if (m <= 0) break;
+  for (int c = 0; c < nch; ++c) {
+    const long long b = bounds[c], m = bounds[c + 1] - bounds[c];
     CB_CUDA(cudaMemcpyAsync(d_points_ws + b * J, h_points + b * J, sizeof(double) * m * J, cudaMemcpyHostToDevice,
                             p->up),
             "cb_eval_points_host");
