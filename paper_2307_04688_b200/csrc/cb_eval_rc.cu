@@ -130,7 +130,8 @@ __global__ void __launch_bounds__(Roles<16>::THREADS, 1)
       const int rbase = blk * kRows + rg * 16 + tq;   // this lane's row at k-step ks: rbase + 4*ks
       // one k-step: 4 rows of the stage; the row digits come straight from FastDiv (no carries),
       // so the fully-valid case below is straight-line code the scheduler can software-pipeline
-      auto kstep = [&](int ks) {
+      // B fragments W[r][p] of k-step ks for this lane's row r and points pcol + 8*nt (zero past R)
+      auto wfrag = [&](int ks, double* w) {
         const int r = rbase + 4 * ks;
         int dig[NL];
         {
@@ -144,8 +145,6 @@ __global__ void __launch_bounds__(Roles<16>::THREADS, 1)
           }
           dig[0] = min(static_cast<int>(rem), p.n[0] - 1);  // r >= R: clamp the lookup (weight is zeroed)
         }
-        // B fragments: W[r][p] for this lane's row r and points pcol + 8*nt (zero past R)
-        double w[NT];
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           double v = Tsb[p.toff[0] + dig[0] * kTP + pcol + nt * 8];
@@ -153,7 +152,9 @@ __global__ void __launch_bounds__(Roles<16>::THREADS, 1)
           for (int d = 1; d < NL; ++d) v *= Tsb[p.toff[d] + dig[d] * kTP + pcol + nt * 8];
           w[nt] = (r < R) ? v : 0.0;
         }
-        // A^T fragments: A[r][mt*8 + gq]
+      };
+      // one k-step: 4 rows of the stage, DMMAs on the DMMA m-tiles + DFMA tail columns
+      auto kstep = [&](int ks, const double* w) {
         double a[MTK];
 #pragma unroll
         for (int m = 0; m < MTK; ++m) a[m] = Ast[ks * 4 * p.kc + m * 8];
@@ -173,11 +174,28 @@ __global__ void __launch_bounds__(Roles<16>::THREADS, 1)
       };
       const int kvalid = min(4, (static_cast<int>(p.R8) - (blk * kRows + rg * 16) + 3) / 4);  // k-steps with rows < R8
       if (kvalid == 4) {
+        // software-pipelined: the next k-step's W products are formed (and pinned in program
+        // order by the volatile asm) before this k-step's DMMAs, hiding the DMUL latency
+        double wc[NT], wn[NT];
+        wfrag(0, wc);
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks) kstep(ks);
+        for (int ks = 0; ks < 4; ++ks) {
+          if (ks + 1 < 4) {
+            wfrag(ks + 1, wn);
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) asm volatile("" : "+d"(wn[nt]));
+          }
+          kstep(ks, wc);
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) wc[nt] = wn[nt];
+        }
       } else {
 #pragma unroll 1
-        for (int ks = 0; ks < kvalid; ++ks) kstep(ks);
+        for (int ks = 0; ks < kvalid; ++ks) {
+          double w[NT];
+          wfrag(ks, w);
+          kstep(ks, w);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_empty[slot]);
