@@ -20,6 +20,7 @@
 // (K1 transform)] pairs in a CUDA graph; the sup-norm change per player is reduced with atomicMax on the IEEE bits
 // (non-negative doubles order like their bit patterns) and the stopping test runs on the device,
 // so the host only polls a flag once per graph launch.
+#include <algorithm>
 #include <cstdio>
 #include <cmath>
 #include "../../include/chebnash_b200.h"
@@ -65,6 +66,8 @@ struct SweepArgs {
   unsigned long long* clamp_base;
   SolveCtl* ctl;                  // solve only
   Status* st;                     // single sweep: non-finite flag
+  int coef_smem;                  // stage all J value tensors in shared memory (one L2 round trip)
+  int drift_blk;                  // doubles per warp of the staged drift block (0: read from L2)
 };
 
 // numpy's pairwise summation for n <= 128 (umath loops: 8 partial sums, then a fixed tree).
@@ -290,26 +293,32 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(const __grid_co
   __shared__ double sQ2[kSweepWarps][kKMax];
   __shared__ double sPt[kSweepWarps][kKMax][kSolverMaxJ];        // successor points (reference coords)
   __shared__ double sTv[kSweepWarps][kSolverMaxJ][kSolverMaxN];  // value basis rows of one successor
+  extern __shared__ __align__(16) double sdyn[];
   const cb_game_t& g = a.g;
   const int J = g.J;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long task = static_cast<long long>(blockIdx.x) * kSweepWarps + warp;
+  const bool done = a.ctl ? (a.ctl->done != 0) : false;  // grid-uniform
+  if (done) {  // converged earlier in this graph launch: carry the fields forward
+    if (task < J * a.NP && lane == 0) {
+      const long long ip = task;
+      a.v_new[ip] = a.v_old[ip];
+      a.u_new[ip] = a.u_old[ip];
+    }
+    return;
+  }
+  // the value tensors of all players, staged once per block (coalesced)
+  double* sC = sdyn;
+  double* sD = sdyn + (a.coef_smem ? J * a.NP : 0);
+  if (a.coef_smem) {
+    for (long long e = threadIdx.x; e < J * a.NP; e += blockDim.x) sC[e] = __ldg(a.coef + e);
+  }
+  __syncthreads();
   if (task >= J * a.NP) return;
   const int i = static_cast<int>(task / a.NP);
   const long long p = task - static_cast<long long>(i) * a.NP;
   const long long ip = static_cast<long long>(i) * a.NP + p;
-
-  long long it = 0;
-  if (a.ctl) {
-    if (a.ctl->done) {  // converged earlier in this graph launch: carry the fields forward
-      if (lane == 0) {
-        a.v_new[ip] = a.v_old[ip];
-        a.u_new[ip] = a.u_old[ip];
-      }
-      return;
-    }
-    it = a.ctl->it;
-  }
+  const long long it = a.ctl ? a.ctl->it : 0;
   const int K = g.nu[i];
   const double u_scale = 2.0 / g.U_max;
   const double p_scale = 2.0 / g.P_max;
@@ -321,6 +330,14 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(const __grid_co
     bdim[t] = t < i ? t : t + 1;
     bsz[t] = g.nu[bdim[t]];
     NB *= bsz[t];
+  }
+  // this node's drift block D_i[p] (NB, K, J), prefetched into shared memory while the basis rows
+  // are formed
+  const double* D = a.drift + a.dofs[i] + static_cast<long long>(p) * NB * K * J;
+  if (a.drift_blk) {
+    double* dst = sD + warp * a.drift_blk;
+    for (long long e = lane; e < NB * K * J; e += 32) dst[e] = __ldg(D + e);
+    D = dst;
   }
   if (lane < J - 1) {
     const double x = a.u_old[static_cast<long long>(bdim[lane]) * a.NP + p] * u_scale - 1.0;
@@ -335,7 +352,6 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(const __grid_co
   //    the node-major layout makes each b a contiguous (K, J) block: coalesced lane reads
   {
     const int KJ = K * J;
-    const double* D = a.drift + a.dofs[i] + static_cast<long long>(p) * NB * KJ;
     for (int r = lane; r < KJ; r += 32) {
       int tt[kSolverMaxJ - 1];
       for (int t = 0; t < J - 1; ++t) tt[t] = 0;
@@ -344,7 +360,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(const __grid_co
       for (int b = 0; b < static_cast<int>(NB); ++b) {
         double w = sT[warp][0][tt[0]];
         for (int t = 1; t < J - 1; ++t) w = w * sT[warp][t][tt[t]];
-        acc = acc + w * __ldg(D + static_cast<long long>(b) * KJ + r);
+        acc = acc + w * D[static_cast<long long>(b) * KJ + r];
         for (int t = J - 2; t >= 0; --t) {  // next bound tuple (last bound player fastest)
           if (++tt[t] < bsz[t]) break;
           tt[t] = 0;
@@ -384,7 +400,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(const __grid_co
   // per point (flat coefficient index split over lanes, T tables in smem, shuffle reduction) when
   // the tensor has more than 128 coefficients
   double vnext = 0.0;
-  const double* Ci = a.coef + static_cast<long long>(i) * a.NP;
+  const double* Ci = (a.coef_smem ? sC : a.coef) + static_cast<long long>(i) * a.NP;
   if (a.NP <= 128) {
     if (lane < K) vnext = eval_reversed(Ci, J, g.np, sPt[warp][lane]);
   } else {
@@ -414,7 +430,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(const __grid_co
       for (long long e = lane; e < a.NP; e += 32) {
         double w = sTv[warp][0][dg[0]];
         for (int d = 1; d < J; ++d) w = w * sTv[warp][d][dg[d]];
-        part = part + w * __ldg(Ci + e);
+        part = part + w * Ci[e];
         int carry = 0;  // flat index += 32 in the mixed radix of the tensor
         for (int d = 0; d < J; ++d) {
           dg[d] += d32[d] + carry;
@@ -651,10 +667,31 @@ long long drift_offsets(const cb_game_t& g, long long* dofs) {
   return total;
 }
 
-cudaError_t launch_sweep(const SweepArgs& a, cudaStream_t s) {
+constexpr int kSweepDynSmem = 160 * 1024;
+
+cudaError_t launch_sweep(SweepArgs a, cudaStream_t s) {
   const long long tasks = a.g.J * a.NP;
   const long long blocks = (tasks + kSweepWarps - 1) / kSweepWarps;
-  sweep_kernel<<<static_cast<unsigned>(blocks), kSweepWarps * 32, 0, s>>>(a);
+  // shared-memory staging: all value tensors (<= 64 KB) and one drift block per warp (<= 24 KB),
+  // used only while the grid still fits in one wave (static smem + staging per block, <= 4 blocks
+  // per SM by registers); otherwise both are read from L2
+  long long blk = 0;
+  for (int i = 0; i < a.g.J; ++i) {
+    long long NB = 1;
+    for (int j = 0; j < a.g.J; ++j)
+      if (j != i) NB *= a.g.nu[j];
+    const long long b = NB * a.g.nu[i] * a.g.J;
+    if (b > blk) blk = b;
+  }
+  const bool coef_ok = tasks * 8 <= 64 * 1024, drift_ok = blk * 8 <= 24 * 1024;
+  const size_t dyn = (coef_ok ? tasks * 8 : 0) + (drift_ok ? blk * 8 * kSweepWarps : 0);
+  const long long per_sm = std::min<long long>(4, (227 * 1024) / (44 * 1024 + static_cast<long long>(dyn)));
+  const bool stage = blocks <= per_sm * num_sms();
+  a.coef_smem = (stage && coef_ok) ? 1 : 0;
+  a.drift_blk = (stage && drift_ok) ? static_cast<int>(blk) : 0;
+  const size_t bytes = stage ? dyn : 0;
+  ensure_smem_attr(reinterpret_cast<const void*>(sweep_kernel), kSweepDynSmem);
+  sweep_kernel<<<static_cast<unsigned>(blocks), kSweepWarps * 32, bytes, s>>>(a);
   count_launch();
   return cudaGetLastError();
 }
