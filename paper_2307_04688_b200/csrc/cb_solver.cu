@@ -112,6 +112,40 @@ __device__ void deriv_row(const double* p, int L, double* q) {
 __device__ __forceinline__ double np_sign(double v) { return v > 0.0 ? 1.0 : (v < 0.0 ? -1.0 : (v == 0.0 ? 0.0 : v)); }
 __device__ __forceinline__ double clip1(double v) { return fmin(fmax(v, -1.0), 1.0); }
 
+// 60 bisection steps on sign(f') (S/solver.py:252-257) as 12 rounds of a depth-5 speculative
+// search: lane j (1..31) evaluates the midpoint of the bracket that sequential bisection would
+// reach at heap node j, a ballot resolves five levels at once.  Every midpoint is formed by the
+// same 0.5*(lo+hi) from the same brackets as the sequential loop, so lo/hi are bitwise identical.
+template <typename F>
+__device__ __forceinline__ void bisect_warp(F&& q1_at, double& lo, double& hi, double s_lo) {
+  const int lane = threadIdx.x & 31;
+  for (int round = 0; round < kBisect / 5; ++round) {
+    bool same = false;
+    if (lane >= 1) {
+      double l = lo, h = hi;
+      const int depth = 31 - __clz(lane);  // path bits below the leading one
+      for (int b = depth - 1; b >= 0; --b) {
+        const double mid = 0.5 * (l + h);
+        if ((lane >> b) & 1) l = mid;
+        else h = mid;
+      }
+      same = np_sign(q1_at(0.5 * (l + h))) == s_lo;
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, same);
+    int node = 1;
+    for (int lev = 0; lev < 5; ++lev) {
+      const double mid = 0.5 * (lo + hi);
+      if ((mask >> node) & 1u) {
+        lo = mid;
+        node = 2 * node + 1;
+      } else {
+        hi = mid;
+        node = 2 * node;
+      }
+    }
+  }
+}
+
 // _maximise_block for one row held in shared memory (c, L); all 32 lanes call it and get the
 // same (x, f).  q1 / q2: per-warp scratch (L-1, L-2).
 __device__ void warp_maximise(const double* c, int L, double x0, bool always_scan, double* q1, double* q2,
@@ -183,12 +217,7 @@ __device__ void warp_maximise(const double* c, int L, double x0, bool always_sca
     double lo = xs_at(bj > 0 ? bj - 1 : 0);
     double hi = xs_at(bj < kScanPoints - 1 ? bj + 1 : kScanPoints - 1);
     const double s_lo = np_sign(clenshaw_row(q1, L - 1, lo));
-    for (int s = 0; s < kBisect; ++s) {
-      const double mid = 0.5 * (lo + hi);
-      const bool same = np_sign(clenshaw_row(q1, L - 1, mid)) == s_lo;
-      if (same) lo = mid;
-      else hi = mid;
-    }
+    bisect_warp([&](double xm) { return clenshaw_row(q1, L - 1, xm); }, lo, hi, s_lo);
     const double x_ref = 0.5 * (lo + hi);
     const double x_fb = (clenshaw_row(c, L, x_ref) >= bv) ? x_ref : x_scan;
     double cf = clenshaw_row(c, L, x_fb);
@@ -204,6 +233,153 @@ __device__ void warp_maximise(const double* c, int L, double x0, bool always_sca
   }
   x_out = best_x;
   f_out = best_f;
+}
+
+// Register-resident form of warp_maximise for a compile-time row length LT (3..16): the same
+// operations in the same order (bitwise identical results), with the coefficient, derivative and
+// second-derivative rows unrolled into registers instead of re-read from shared memory.
+template <int LT>
+__device__ __forceinline__ double clen_t(const double* c, double x) {
+  if constexpr (LT == 1) {
+    return c[0];
+  } else {
+    const double x2 = 2.0 * x;
+    double b1 = 0.0, b2 = 0.0;
+#pragma unroll
+    for (int k = LT - 1; k >= 1; --k) {
+      const double t = c[k] + x2 * b1 - b2;
+      b2 = b1;
+      b1 = t;
+    }
+    return c[0] + x * b1 - b2;
+  }
+}
+
+template <int LT>
+__device__ __forceinline__ double np_sum_t(const double* a) {
+  if constexpr (LT < 8) {
+    double r = 0.0;
+#pragma unroll
+    for (int i = 0; i < LT; ++i) r = r + a[i];
+    return r;
+  } else {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    constexpr int full = LT - (LT % 8);
+#pragma unroll
+    for (int i = 8; i < full; i += 8)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = r[j] + a[i + j];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+#pragma unroll
+    for (int i = full; i < LT; ++i) res = res + a[i];
+    return res;
+  }
+}
+
+template <int LT>
+__device__ __forceinline__ void deriv_t(const double* p, double* q) {
+  constexpr int n = LT - 1;
+  q[n - 1] = 2.0 * n * p[n];
+  if constexpr (n >= 2) q[n - 2] = 2.0 * (n - 1) * p[n - 1];
+#pragma unroll
+  for (int l = n - 3; l >= 0; --l) q[l] = q[l + 2] + 2.0 * (l + 1) * p[l + 1];
+  q[0] *= 0.5;
+}
+
+template <int LT>
+__device__ void warp_maximise_t(const double* cs, double x0, bool always_scan, double& x_out, double& f_out) {
+  const int lane = threadIdx.x & 31;
+  double c[LT], alt[LT], q1[LT - 1], q2[LT - 2];
+#pragma unroll
+  for (int l = 0; l < LT; ++l) {
+    c[l] = cs[l];
+    alt[l] = (l & 1) ? -c[l] : c[l];
+  }
+  const double f_hi = np_sum_t<LT>(c);
+  const double f_lo = np_sum_t<LT>(alt);
+  deriv_t<LT>(c, q1);
+  deriv_t<LT - 1>(q1, q2);
+  double x = clip1(x0);
+  bool moving = true, failed = false;
+  for (int it = 0; it < kNewtonIter; ++it) {
+    const double f1 = clen_t<LT - 1>(q1, x);
+    const double f2 = clen_t<LT - 2>(q2, x);
+    const bool tiny = fabs(f2) <= 1e-300;
+    const double raw = x - f1 / (tiny ? 1.0 : f2);
+    const double xn = clip1(raw);
+    if (moving && ((!tiny && raw != xn) || tiny)) failed = true;
+    moving = moving && !tiny;
+    const double dx = fabs(xn - x);
+    if (moving) x = xn;
+    moving = moving && (dx > kNewtonTol);
+    if (!moving) break;
+  }
+  failed = failed || moving;
+  failed = failed || (clen_t<LT - 2>(q2, x) >= 0.0);
+  if (always_scan) failed = true;
+  double best_x = x, best_f = clen_t<LT>(c, x);
+  if (f_lo > best_f) {
+    best_x = -1.0;
+    best_f = f_lo;
+  }
+  if (f_hi > best_f) {
+    best_x = 1.0;
+    best_f = f_hi;
+  }
+  if (failed) {
+    double bv = -INFINITY;
+    int bj = kScanPoints;
+    for (int j = lane; j < kScanPoints; j += 32) {
+      const double xs = (j == kScanPoints - 1) ? 1.0 : -1.0 + j * (2.0 / (kScanPoints - 1));
+      const double v = clen_t<LT>(c, xs);
+      if (v > bv || bj == kScanPoints) {
+        bv = v;
+        bj = j;
+      }
+    }
+    for (int o = 16; o >= 1; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+      if (ov > bv || (ov == bv && oj < bj)) {
+        bv = ov;
+        bj = oj;
+      }
+    }
+    auto xs_at = [](int j) { return (j == kScanPoints - 1) ? 1.0 : -1.0 + j * (2.0 / (kScanPoints - 1)); };
+    const double x_scan = xs_at(bj);
+    double lo = xs_at(bj > 0 ? bj - 1 : 0);
+    double hi = xs_at(bj < kScanPoints - 1 ? bj + 1 : kScanPoints - 1);
+    const double s_lo = np_sign(clen_t<LT - 1>(q1, lo));
+    bisect_warp([&](double xm) { return clen_t<LT - 1>(q1, xm); }, lo, hi, s_lo);
+    const double x_ref = 0.5 * (lo + hi);
+    const double x_fb = (clen_t<LT>(c, x_ref) >= bv) ? x_ref : x_scan;
+    double cf = clen_t<LT>(c, x_fb);
+    if (cf > best_f) {
+      best_x = x_fb;
+      best_f = cf;
+    }
+    cf = clen_t<LT>(c, x_scan);
+    if (cf > best_f) {
+      best_x = x_scan;
+      best_f = cf;
+    }
+  }
+  x_out = best_x;
+  f_out = best_f;
+}
+
+// row-length dispatch: registers for 3 <= L <= 16, the shared-memory form otherwise
+__device__ void warp_maximise_any(const double* c, int L, double x0, bool always_scan, double* q1, double* q2,
+                                  double& x_out, double& f_out) {
+  switch (L) {
+#define CB_MX(v) case v: warp_maximise_t<v>(c, x0, always_scan, x_out, f_out); return;
+    CB_MX(3) CB_MX(4) CB_MX(5) CB_MX(6) CB_MX(7) CB_MX(8) CB_MX(9) CB_MX(10) CB_MX(11) CB_MX(12) CB_MX(13)
+    CB_MX(14) CB_MX(15) CB_MX(16)
+#undef CB_MX
+    default: warp_maximise(c, L, x0, always_scan, q1, q2, x_out, f_out); return;
+  }
 }
 
 // Value interpolant of one player at a point: coefficients with reversed axes (l_J, ..., l_1),
@@ -324,11 +500,13 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(const __grid_co
   const double p_scale = 2.0 / g.P_max;
 
   // 1. basis rows of the bound players' current controls at this node (Step 1, :374-379)
+  //    (small per-player arrays are indexed only by unrolled constants -> registers)
   int bsz[kSolverMaxJ - 1], bdim[kSolverMaxJ - 1];
   long long NB = 1;
-  for (int t = 0; t < J - 1; ++t) {
+#pragma unroll
+  for (int t = 0; t < kSolverMaxJ - 1; ++t) {
     bdim[t] = t < i ? t : t + 1;
-    bsz[t] = g.nu[bdim[t]];
+    bsz[t] = (t < J - 1) ? g.nu[bdim[t]] : 1;
     NB *= bsz[t];
   }
   // this node's drift block D_i[p] (NB, K, J), prefetched into shared memory while the basis rows
@@ -340,12 +518,14 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(const __grid_co
     D = dst;
   }
   if (lane < J - 1) {
-    const double x = a.u_old[static_cast<long long>(bdim[lane]) * a.NP + p] * u_scale - 1.0;
+    const int bd = lane < i ? lane : lane + 1;
+    const int bs = g.nu[bd];
+    const double x = a.u_old[static_cast<long long>(bd) * a.NP + p] * u_scale - 1.0;
     double* row = sT[warp][lane];
     row[0] = 1.0;
-    if (bsz[lane] > 1) row[1] = x;
+    if (bs > 1) row[1] = x;
     const double x2 = 2.0 * x;
-    for (int l = 2; l < bsz[lane]; ++l) row[l] = x2 * row[l - 1] - row[l - 2];
+    for (int l = 2; l < bs; ++l) row[l] = x2 * row[l - 1] - row[l - 2];
   }
   __syncwarp();
   // 2. bind: acc[l_own * J + comp] = sum over bound tuples b of prod T * D_i[p][b][l_own][comp];
@@ -354,16 +534,23 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(const __grid_co
     const int KJ = K * J;
     for (int r = lane; r < KJ; r += 32) {
       int tt[kSolverMaxJ - 1];
-      for (int t = 0; t < J - 1; ++t) tt[t] = 0;
+#pragma unroll
+      for (int t = 0; t < kSolverMaxJ - 1; ++t) tt[t] = 0;
       double acc = 0.0;
-#pragma unroll 8
+#pragma unroll 4
       for (int b = 0; b < static_cast<int>(NB); ++b) {
         double w = sT[warp][0][tt[0]];
-        for (int t = 1; t < J - 1; ++t) w = w * sT[warp][t][tt[t]];
+#pragma unroll
+        for (int t = 1; t < kSolverMaxJ - 1; ++t)
+          if (t < J - 1) w = w * sT[warp][t][tt[t]];
         acc = acc + w * D[static_cast<long long>(b) * KJ + r];
-        for (int t = J - 2; t >= 0; --t) {  // next bound tuple (last bound player fastest)
-          if (++tt[t] < bsz[t]) break;
-          tt[t] = 0;
+        bool carry = true;  // next bound tuple (last bound player fastest)
+#pragma unroll
+        for (int t = kSolverMaxJ - 2; t >= 0; --t) {
+          if (carry && t < J - 1) {
+            if (++tt[t] < bsz[t]) carry = false;
+            else tt[t] = 0;
+          }
         }
       }
       sAcc[warp][r] = acc;
@@ -376,7 +563,8 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(const __grid_co
     const int k = lane;
     const double rn = g.rnodes[i][k];
     double gk[kSolverMaxJ];
-    for (int c = 0; c < J; ++c) gk[c] = 0.0;
+#pragma unroll
+    for (int c = 0; c < kSolverMaxJ; ++c) gk[c] = 0.0;
     double T0 = 1.0, T1 = rn;
     for (int l = 0; l < K; ++l) {
       const double Tl = (l == 0) ? 1.0 : (l == 1 ? rn : (2.0 * rn) * T1 - T0);
@@ -384,16 +572,19 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(const __grid_co
         T0 = T1;
         T1 = Tl;
       }
-      for (int c = 0; c < J; ++c) gk[c] = gk[c] + Tl * sAcc[warp][l * J + c];
+#pragma unroll
+      for (int c = 0; c < kSolverMaxJ; ++c)
+        if (c < J) gk[c] = gk[c] + Tl * sAcc[warp][l * J + c];
     }
-    double pt[kSolverMaxJ];
-    for (int c = 0; c < J; ++c) {
-      const double nxt = a.nodes[p * J + c] + g.h * gk[c];
-      const double cl = fmin(fmax(nxt, 0.0), g.P_max);
-      clamped += (cl != nxt) ? 1u : 0u;
-      pt[c] = cl * p_scale - 1.0;
+#pragma unroll
+    for (int c = 0; c < kSolverMaxJ; ++c) {
+      if (c < J) {
+        const double nxt = a.nodes[p * J + c] + g.h * gk[c];
+        const double cl = fmin(fmax(nxt, 0.0), g.P_max);
+        clamped += (cl != nxt) ? 1u : 0u;
+        sPt[warp][k][c] = cl * p_scale - 1.0;
+      }
     }
-    for (int c = 0; c < J; ++c) sPt[warp][k][c] = pt[c];
   }
   __syncwarp();
   // value interpolant at the K successors: one lane per point for small tensors; the whole warp
@@ -487,7 +678,7 @@ __global__ void __launch_bounds__(kSweepWarps * 32) sweep_kernel(const __grid_co
   __syncwarp();
   // 5. maximise from the warm start
   double xb, fb;
-  warp_maximise(sCoef[warp], K, a.u_old[ip] * u_scale - 1.0, false, sQ1[warp], sQ2[warp], xb, fb);
+  warp_maximise_any(sCoef[warp], K, a.u_old[ip] * u_scale - 1.0, false, sQ1[warp], sQ2[warp], xb, fb);
   for (int o = 16; o >= 1; o >>= 1) clamped += __shfl_xor_sync(0xffffffffu, clamped, o);
   if (lane == 0) {
     a.u_new[ip] = (xb + 1.0) * (0.5 * g.U_max);
@@ -527,7 +718,7 @@ __global__ void maximise_rows_kernel(long long m, int L, const double* coef, con
   if (lane < L) sC[warp][lane] = coef[row * L + lane];
   __syncwarp();
   double xb, fb;
-  warp_maximise(sC[warp], L, x0[row], always_scan != 0, sQ1[warp], sQ2[warp], xb, fb);
+  warp_maximise_any(sC[warp], L, x0[row], always_scan != 0, sQ1[warp], sQ2[warp], xb, fb);
   if (lane == 0) {
     x[row] = xb;
     f[row] = fb;
