@@ -838,6 +838,45 @@ __global__ void drift_layout_kernel(const __grid_constant__ cb_game_t g, long lo
   drift[e] = stacks[comp * selems + off * NP + p];
 }
 
+
+// Refit of small value fields in ONE launch (instead of one fiber pass per mode): block b
+// transforms player b's node values (np_J, ..., np_1 as C order, dim 1 fastest) along every mode
+// in shared memory with the unfolded DCT-I matrix (transform_entry, exact angle reduction) and
+// writes the reversed-axis coefficient tensor.  Used when N_P <= 4096 and every np_d <= 64.
+constexpr int kRefitThreads = 256;
+
+__global__ void __launch_bounds__(kRefitThreads) refit_small_kernel(const __grid_constant__ cb_game_t g, long long NP,
+                                                                    const double* __restrict__ v,
+                                                                    double* __restrict__ coef) {
+  extern __shared__ __align__(16) double rs[];
+  double* A = rs;             // [NP]
+  double* B = rs + NP;        // [NP]
+  double* M = rs + 2 * NP;    // [64 * 64] matrix of the current mode
+  const int i = blockIdx.x;
+  for (long long e = threadIdx.x; e < NP; e += blockDim.x) A[e] = v[i * NP + e];
+  long long stride = 1;  // element stride of dim d (dim 0 fastest)
+  for (int d = 0; d < g.J; ++d) {
+    const int n = g.np[d], N = n - 1;
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) M[e] = transform_entry(e / n, e % n, N);
+    __syncthreads();
+    const long long fibers = NP / n;
+    for (long long f = threadIdx.x; f < fibers * n; f += blockDim.x) {
+      const long long fib = f / n;
+      const int l = static_cast<int>(f - fib * n);
+      const long long base = (fib / stride) * stride * n + (fib % stride);
+      double acc = 0.0;
+      for (int k = 0; k < n; ++k) acc = fma(M[l * n + k], A[base + k * stride], acc);
+      B[base + l * stride] = acc;
+    }
+    __syncthreads();
+    double* t = A;
+    A = B;
+    B = t;
+    stride *= n;
+  }
+  for (long long e = threadIdx.x; e < NP; e += blockDim.x) coef[i * NP + e] = A[e];
+}
+
 long long nodes_of(const cb_game_t& g) {
   long long n = 1;
   for (int d = 0; d < g.J; ++d) n *= g.np[d];
@@ -890,6 +929,16 @@ cudaError_t launch_sweep(SweepArgs a, cudaStream_t s) {
 // refit (S/solver.py:441-449): node values (J, N_P) viewed as (J, np_J, ..., np_1) -> reversed-axis
 // coefficient tensors, one K1 transform over axes 1..J
 cudaError_t refit(const cb_game_t& g, const double* v, double* coef, cudaStream_t s) {
+  const long long NP = nodes_of(g);
+  bool small = NP <= 4096;
+  for (int d = 0; d < g.J; ++d) small = small && g.np[d] <= 64;
+  if (small) {
+    const size_t bytes = sizeof(double) * (2 * NP + 64 * 64);
+    ensure_smem_attr(reinterpret_cast<const void*>(refit_small_kernel), static_cast<int>(bytes));
+    refit_small_kernel<<<g.J, kRefitThreads, bytes, s>>>(g, NP, v, coef);
+    count_launch();
+    return cudaGetLastError();
+  }
   long long shape[kSolverMaxJ + 1];
   shape[0] = g.J;
   for (int d = 0; d < g.J; ++d) shape[1 + d] = g.np[g.J - 1 - d];
