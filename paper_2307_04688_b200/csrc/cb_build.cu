@@ -389,6 +389,76 @@ __global__ void __launch_bounds__(kFiberThreads) fiber_pass_kernel(const __grid_
   }
 }
 
+
+// Innermost-mode fiber pass (unit stride in and out): a block stages 128 consecutive fibers
+// (contiguous 128*TN doubles of the dense input) through shared memory, so global loads and the
+// row stores are coalesced instead of each lane walking its own TN-element fiber.
+template <int TN>
+__global__ void __launch_bounds__(kFiberThreads) fiber_inner_kernel(const __grid_constant__ FiberParams p) {
+  __shared__ double buf[kFiberThreads * TN];
+  __shared__ long long ooff[kFiberThreads];
+  const long long f0 = static_cast<long long>(blockIdx.x) * kFiberThreads;
+  const int nf = static_cast<int>(min(static_cast<long long>(kFiberThreads), p.fibers - f0));
+  // fiber f's input offset is f*TN (dense, innermost mode); output offset via the other-dim strides
+  {
+    const long long f = f0 + threadIdx.x;
+    long long oout = 0;
+    if (threadIdx.x < nf) {
+      uint32_t rem = static_cast<uint32_t>(f);
+#pragma unroll
+      for (int i = kMaxDims; i >= 0; --i) {
+        if (i < p.nother) {
+          uint32_t q, r;
+          p.fd[i].divmod(rem, q, r);
+          oout += static_cast<long long>(r) * p.sout[i];
+          rem = q;
+        }
+      }
+    }
+    ooff[threadIdx.x] = oout;
+  }
+  const double* src = p.in + f0 * TN;
+  for (int e = threadIdx.x; e < nf * TN; e += kFiberThreads) buf[e] = src[e];
+  __syncthreads();
+  if (threadIdx.x < nf) {
+    constexpr int N = TN - 1, H = TN / 2, P = H + 1;
+    double v[TN];
+    double* row = buf + threadIdx.x * TN;
+#pragma unroll
+    for (int k = 0; k < TN; ++k) v[k] = row[k];
+    if (p.check_finite) {
+      bool ok = true;
+#pragma unroll
+      for (int k = 0; k < TN; ++k) ok &= isfinite(v[k]);
+      if (!ok) atomicAdd(&p.st->nonfinite, 1u);
+    }
+    double e[H > 0 ? H : 1], o[H > 0 ? H : 1];
+#pragma unroll
+    for (int k = 0; k < H; ++k) {
+      e[k] = v[k] + v[N - k];
+      o[k] = v[k] - v[N - k];
+    }
+#pragma unroll
+    for (int l = 0; l <= N; ++l) {
+      double acc = 0.0;
+      if ((l & 1) == 0) {
+#pragma unroll
+        for (int k = 0; k < H; ++k) acc = fma(p.M[l * P + k], e[k], acc);
+        if constexpr (TN & 1) acc = fma(p.M[l * P + H], v[H], acc);
+      } else {
+#pragma unroll
+        for (int k = 0; k < H; ++k) acc = fma(p.M[l * P + k], o[k], acc);
+      }
+      row[l] = acc;
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nf * TN; e += kFiberThreads) {
+    const int fl = e / TN, l = e - (e / TN) * TN;
+    p.out[ooff[fl] + l] = buf[e];
+  }
+}
+
 template <int TN>
 struct FTag { static constexpr int value = TN; };
 
@@ -439,9 +509,19 @@ bool launch_fiber_pass(int nd, const long long* sizes, const long long* sin, con
   const long long grid = (fibers + kFiberThreads - 1) / kFiberThreads;
   *err = cudaSuccess;
   if (grid <= 0) return true;
+  // innermost mode with a dense input and unit output stride: shared-memory staged variant
+  bool dense_in = p.kin == 1 && p.kout == 1 && n >= 2;
+  if (dense_in) {
+    long long expect = n;  // input strides of the other dims must be those of a dense C array
+    for (int i = j - 1; i >= 0; --i) {
+      dense_in = dense_in && p.sin[i] == expect;
+      expect *= p.nd[i];
+    }
+  }
   dispatch_fiber(n, [&](auto tag) {
     constexpr int TN = decltype(tag)::value;
-    fiber_pass_kernel<TN><<<static_cast<unsigned>(grid), kFiberThreads, 0, stream>>>(p);
+    if (dense_in && TN >= 2) fiber_inner_kernel<TN><<<static_cast<unsigned>(grid), kFiberThreads, 0, stream>>>(p);
+    else fiber_pass_kernel<TN><<<static_cast<unsigned>(grid), kFiberThreads, 0, stream>>>(p);
   });
   count_launch();
   *err = cudaGetLastError();
