@@ -37,7 +37,8 @@ extern "C" {
 enum {
   CB_OK = 0,
   CB_EINVAL = 1,     /* bad shape / argument (reference raises ValueError) */
-  CB_ENONFINITE = 2, /* non-finite objective sample in a Bellman sweep (FloatingPointError) */
+  CB_ENONFINITE = 2, /* non-finite objective in a sweep / non-concave LQ update (FloatingPointError) */
+  CB_ENOFIX = 3,     /* LQ coefficient iteration did not settle (RuntimeError) */
   CB_ECUDA = 4       /* CUDA runtime error */
 };
 
@@ -211,6 +212,15 @@ int cb_solve(const cb_game_t* game, const double* d_nodes, const double* d_drift
  * (np_1..np_J) each, concatenated; d_p0 (batch, J); d_states, d_controls (batch, n_steps+1, J). */
 int cb_simulate(const cb_game_t* game, int64_t batch, const double* d_policies, const double* d_p0, int64_t n_steps,
                 double* d_states, double* d_controls, void* stream);
+
+/* Closed-form linear-quadratic equilibrium (the reference's validation oracle, oracle.py:65-163):
+ * d_state = [Q (J,J,J)][b (J,J)][d (J)][e (J)][f (J,J)] (device doubles).  mode 0: one exact
+ * Bellman update of d_state (lq_bellman_update); mode 1: lq_solve from the zero value function
+ * (iterate until the (Q, b, e, f) change < tol, then close the constant term).  d_work holds
+ * J^3 + 2J^2 + 2J doubles + 16 bytes.  Synchronous (returns the iteration count).  Errors:
+ * CB_ENONFINITE (not concave), CB_ENOFIX (no fixed point within max_iters). */
+int cb_lq(const cb_game_t* game, double* d_state, double* d_work, int64_t max_iters, double tol, int mode,
+          int64_t* iterations, void* stream);
 
 /* Safeguarded maximiser _maximise_block (solver.py:262-323) on m rows of L coefficients
  * (reference variable on [-1, 1]) from warm starts d_x0: d_x, d_f (m,).  always_scan != 0 adds the

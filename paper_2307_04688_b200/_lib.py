@@ -86,6 +86,7 @@ SIGNATURES = {
     "cb_solve": (_c_int, [_gamep, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _i64p, ctypes.POINTER(_c_int), _vp]),
     "cb_maximise_rows": (_c_int, [_c_i64, _c_int, _vp, _vp, _vp, _vp, _c_int, _vp]),
     "cb_simulate": (_c_int, [_gamep, _c_i64, _vp, _vp, _c_i64, _vp, _vp, _vp]),
+    "cb_lq": (_c_int, [_gamep, _vp, _vp, _c_i64, _c_dbl, _c_int, _i64p, _vp]),
 }
 
 _lib = None
@@ -124,6 +125,8 @@ def check(rc: int, what: str = "") -> None:
             raise ValueError(msg or what)
         if rc == 2:
             raise FloatingPointError(msg or what)
+        if rc == 3:
+            raise RuntimeError(msg or what)
         raise CudaLibraryError(f"{what}: {msg}" if what else msg)
 
 

@@ -556,3 +556,17 @@ int cb_simulate(const cb_game_t* game, int64_t batch, const double* d_policies, 
           "cb_simulate");
   return CB_OK;
 }
+
+int cb_lq(const cb_game_t* game, double* d_state, double* d_work, int64_t max_iters, double tol, int mode,
+          int64_t* iterations, void* stream) {
+  int rc = check_game(game, "cb_lq");
+  if (rc) return rc;
+  long long its = 0;
+  int status = 0;
+  CB_CUDA(lq(*game, d_state, d_work, max_iters, tol, mode, &its, &status, static_cast<cudaStream_t>(stream)), "cb_lq");
+  *iterations = its;
+  if (status == 1) return fail(CB_ENONFINITE, "interior maximisation is not concave");
+  if (status == 2) return fail(CB_ENOFIX, "quadratic fixed point not reached in " + std::to_string(max_iters) +
+                                             " iterations");
+  return CB_OK;
+}

@@ -77,6 +77,8 @@ cudaError_t solve(const cb_game_t& g, const double* nodes, const double* drift, 
                   cudaStream_t stream);
 cudaError_t simulate(const cb_game_t& g, long long B, const double* policies, const double* p0, long long n_steps,
                      double* states, double* controls, cudaStream_t stream);
+cudaError_t lq(const cb_game_t& g, double* state, double* work, long long max_iters, double tol, int mode,
+               long long* iterations, int* status, cudaStream_t stream);
 cudaError_t maximise_rows(long long m, int L, const double* coef, const double* x0, double* x, double* f,
                           int always_scan, cudaStream_t stream);
 

@@ -877,6 +877,177 @@ __global__ void __launch_bounds__(kRefitThreads) refit_small_kernel(const __grid
   for (long long e = threadIdx.x; e < NP; e += blockDim.x) coef[i * NP + e] = A[e];
 }
 
+
+// Closed-form linear-quadratic equilibrium (the reference's validation oracle, S/oracle.py:65-163):
+// the exact Bellman update of quadratic values V_i = p'Q_i p + b_i'p + d_i and affine feedback
+// u_i = e_i + f_i'p, iterated in coefficient space on one thread (J <= 8: a few hundred flops per
+// update).  State vector: [Q (J,J,J)][b (J,J)][d (J)][e (J)][f (J,J)].
+struct LQOut {
+  long long iterations;
+  int status;  // 0 ok, 1 interior maximisation not concave, 2 no fixed point within max_iters
+  int pad;
+};
+
+__device__ int lq_update(const cb_game_t& g, const double* Q, const double* b, const double* d, const double* e,
+                         const double* f, double* Qn, double* bn, double* dn, double* en, double* fn) {
+  const int J = g.J;
+  const double h = g.h, delta = g.delta;
+  double D[kSolverMaxJ][kSolverMaxJ];
+  for (int r = 0; r < J; ++r) {
+    double rs = 0.0;
+    for (int c = 0; c < J; ++c) rs = rs + g.K[r][c];
+    for (int c = 0; c < J; ++c) D[r][c] = (g.K[r][c] - (r == c ? rs : 0.0)) / g.m[r] - (r == c ? g.c[r] : 0.0);
+  }
+  for (int i = 0; i < J; ++i) {
+    const double* Qi = Q + i * J * J;
+    const double* bi = b + i * J;
+    double M[kSolverMaxJ][kSolverMaxJ], w[kSolverMaxJ], z[kSolverMaxJ];
+    for (int r = 0; r < J; ++r) {
+      const double Er = (r != i) ? e[r] : 0.0;
+      w[r] = h * g.beta[r] * Er;
+      z[r] = (r == i) ? h * g.beta[i] : 0.0;
+      for (int c = 0; c < J; ++c) {
+        const double Frc = (r != i) ? f[r * J + c] : 0.0;
+        M[r][c] = (r == c ? 1.0 : 0.0) + h * (D[r][c] + g.beta[r] * Frc);
+      }
+    }
+    // z'Qi z, z'Qi (row vector), Qi w
+    double zQ[kSolverMaxJ], Qw[kSolverMaxJ];
+    for (int c = 0; c < J; ++c) {
+      double s1 = 0.0, s2 = 0.0;
+      for (int r = 0; r < J; ++r) {
+        s1 = s1 + z[r] * Qi[r * J + c];
+        s2 = s2 + Qi[c * J + r] * w[r];
+      }
+      zQ[c] = s1;
+      Qw[c] = s2;
+    }
+    double zQz = 0.0;
+    for (int c = 0; c < J; ++c) zQz = zQz + zQ[c] * z[c];
+    const double denom = h - 2.0 * zQz;
+    if (!(denom > 0.0)) return 1;
+    double t = 0.0;
+    for (int r = 0; r < J; ++r) t = t + z[r] * (2.0 * Qw[r] + bi[r]);
+    const double e_new = (h * g.A[i] + t) / denom;
+    double f_new[kSolverMaxJ];
+    for (int c = 0; c < J; ++c) {
+      double s = 0.0;
+      for (int r = 0; r < J; ++r) s = s + (2.0 * zQ[r]) * M[r][c];
+      f_new[c] = s / denom;
+    }
+    double Mt[kSolverMaxJ][kSolverMaxJ], wt[kSolverMaxJ];
+    for (int r = 0; r < J; ++r) {
+      wt[r] = w[r] + e_new * z[r];
+      for (int c = 0; c < J; ++c) Mt[r][c] = M[r][c] + z[r] * f_new[c];
+    }
+    // Qn_i = delta * (h * stage_quad + Mt' Qi Mt), symmetrised
+    double QM[kSolverMaxJ][kSolverMaxJ];
+    for (int r = 0; r < J; ++r)
+      for (int c = 0; c < J; ++c) {
+        double s = 0.0;
+        for (int k = 0; k < J; ++k) s = s + Qi[r * J + k] * Mt[k][c];
+        QM[r][c] = s;
+      }
+    double* Qo = Qn + i * J * J;
+    for (int r = 0; r < J; ++r)
+      for (int c = 0; c < J; ++c) {
+        double s = 0.0;
+        for (int k = 0; k < J; ++k) s = s + Mt[k][r] * QM[k][c];
+        double sq = -0.5 * f_new[r] * f_new[c];
+        if (r == i && c == i) sq -= 0.5 * g.phi[i];
+        Qo[r * J + c] = delta * (h * sq + s);
+      }
+    for (int r = 0; r < J; ++r)
+      for (int c = r + 1; c < J; ++c) {
+        const double a = 0.5 * (Qo[r * J + c] + Qo[c * J + r]);
+        Qo[r * J + c] = a;
+        Qo[c * J + r] = a;
+      }
+    // bn_i = delta * (h (A_i - e_new) f_new + Mt' (2 Qi wt + bi))
+    double v2[kSolverMaxJ];
+    for (int r = 0; r < J; ++r) {
+      double s = 0.0;
+      for (int k = 0; k < J; ++k) s = s + Qi[r * J + k] * wt[k];
+      v2[r] = 2.0 * s + bi[r];
+    }
+    for (int c = 0; c < J; ++c) {
+      double s = 0.0;
+      for (int k = 0; k < J; ++k) s = s + Mt[k][c] * v2[k];
+      bn[i * J + c] = delta * (h * (g.A[i] - e_new) * f_new[c] + s);
+    }
+    double wQw = 0.0, bw = 0.0;
+    for (int r = 0; r < J; ++r) {
+      double s = 0.0;
+      for (int k = 0; k < J; ++k) s = s + Qi[r * J + k] * wt[k];
+      wQw = wQw + wt[r] * s;
+      bw = bw + bi[r] * wt[r];
+    }
+    dn[i] = delta * (h * (g.A[i] * e_new - 0.5 * e_new * e_new) + wQw + bw + d[i]);
+    en[i] = e_new;
+    for (int c = 0; c < J; ++c) fn[i * J + c] = f_new[c];
+  }
+  return 0;
+}
+
+// mode 0: one update of `state`; mode 1: lq_solve from the zero value function (S/oracle.py:112-163)
+__global__ void lq_kernel(const __grid_constant__ cb_game_t g, double* state, double* work, long long max_iters,
+                          double tol, int mode, LQOut* res) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int J = g.J;
+  const int nQ = J * J * J, nb = J * J;
+  const int n = nQ + 2 * nb + 2 * J;
+  double* cur = state;
+  double* nxt = work;
+  auto parts = [&](double* base, double*& Q, double*& b, double*& d, double*& e, double*& f) {
+    Q = base;
+    b = base + nQ;
+    d = b + nb;
+    e = d + J;
+    f = e + J;
+  };
+  double *Q, *b, *d, *e, *f, *Qn, *bn, *dn, *en, *fn;
+  parts(cur, Q, b, d, e, f);
+  parts(nxt, Qn, bn, dn, en, fn);
+  res->status = 0;
+  res->iterations = 0;
+  if (mode == 0) {
+    res->status = lq_update(g, Q, b, d, e, f, Qn, bn, dn, en, fn);
+    for (int k = 0; k < n; ++k) cur[k] = nxt[k];
+    res->iterations = 1;
+    return;
+  }
+  for (int k = 0; k < n; ++k) cur[k] = 0.0;
+  for (int i = 0; i < J; ++i) e[i] = g.A[i];
+  long long it = 1;
+  bool settled = false;
+  for (; it <= max_iters; ++it) {
+    const int st = lq_update(g, Q, b, d, e, f, Qn, bn, dn, en, fn);
+    if (st) {
+      res->status = st;
+      res->iterations = it;
+      return;
+    }
+    double change = 0.0;
+    for (int k = 0; k < nQ + nb; ++k) change = fmax(change, fabs(nxt[k] - cur[k]));
+    for (int k = nQ + nb + J; k < n; ++k) change = fmax(change, fabs(nxt[k] - cur[k]));
+    for (int k = 0; k < n; ++k) cur[k] = nxt[k];
+    if (change < tol) {
+      settled = true;
+      break;
+    }
+  }
+  if (!settled) {
+    res->status = 2;
+    res->iterations = max_iters;
+    return;
+  }
+  // constant term: one update from d = 0, then d_i = d_once_i / (1 - delta)
+  for (int i = 0; i < J; ++i) d[i] = 0.0;
+  res->status = lq_update(g, Q, b, d, e, f, Qn, bn, dn, en, fn);
+  for (int i = 0; i < J; ++i) d[i] = dn[i] / (1.0 - g.delta);
+  res->iterations = it;
+}
+
 long long nodes_of(const cb_game_t& g) {
   long long n = 1;
   for (int d = 0; d < g.J; ++d) n *= g.np[d];
@@ -1077,6 +1248,20 @@ cudaError_t simulate(const cb_game_t& g, long long B, const double* policies, co
                                                                                controls);
   count_launch();
   return cudaGetLastError();
+}
+
+cudaError_t lq(const cb_game_t& g, double* state, double* work, long long max_iters, double tol, int mode,
+               long long* iterations, int* status, cudaStream_t stream) {
+  LQOut* dres = reinterpret_cast<LQOut*>(work + (g.J * g.J * g.J + 2 * g.J * g.J + 2 * g.J));
+  lq_kernel<<<1, 32, 0, stream>>>(g, state, work, max_iters, tol, mode, dres);
+  count_launch();
+  LQOut h{};
+  cudaError_t e = cudaMemcpyAsync(&h, dres, sizeof(h), cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) return e;
+  *iterations = h.iterations;
+  *status = h.status;
+  return cudaSuccess;
 }
 
 cudaError_t maximise_rows(long long m, int L, const double* coef, const double* x0, double* x, double* f,

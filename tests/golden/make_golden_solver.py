@@ -128,6 +128,34 @@ def main():
         out[f"maxblock{L}_x"] = xb
         out[f"maxblock{L}_f"] = fb
 
+    # the closed-form LQ oracle (S/oracle.py): full solves and one exact update from a random state
+    from chebnash import oracle as ro
+
+    for key, preset, kw in (("lq1", "example1", dict(FAST, Np=2, Nu=2)), ("lq2", "example1", {}),
+                            ("lq3", "example3", dict(FAST)), ("lq4", "example4", {})):
+        spec = ref.preset_spec(preset, **kw)
+        spec_arrays(key, spec, out)
+        fb = ro.lq_solve(spec)
+        for name in ("Q", "b", "d", "e", "f"):
+            out[f"{key}_{name}"] = np.asarray(getattr(fb, name))
+        out[f"{key}_iterations"] = np.array(fb.iterations)
+        out[f"{key}_negfrac"] = np.array(fb.negative_fraction)
+        out[f"{key}_highfrac"] = np.array(fb.high_fraction)
+        J = spec.J
+        st = [0.01 * rng.standard_normal((J, J, J)), 0.01 * rng.standard_normal((J, J)),
+              0.01 * rng.standard_normal(J), rng.uniform(0.1, 0.4, J), 0.1 * rng.standard_normal((J, J))]
+        st[0] = 0.5 * (st[0] + np.transpose(st[0], (0, 2, 1)))
+        upd = ro.lq_bellman_update(spec, *st)
+        for name, a, b in zip(("Q", "b", "d", "e", "f"), st, upd):
+            out[f"{key}_upd_in_{name}"] = a
+            out[f"{key}_upd_out_{name}"] = b
+        print(key, "lq iterations", fb.iterations, fb.negative_fraction)
+    # policy error of the e1b solve against its oracle (acceptance #6 machinery)
+    spec = ref.preset_spec("example1", **dict(FAST, Np=3, Nu=3))
+    grid = ref.build_state_grid(spec)
+    res = quiet_solve(spec)
+    out["perr_e1b"] = np.array(ro.policy_error(res.policy, ro.lq_solve(spec, grid), grid))
+
     np.savez_compressed(os.path.join(HERE, "golden_solver_v1.npz"), **out)
     print("wrote", len(out), "arrays")
 
