@@ -231,3 +231,19 @@ def test_acceptance_value_consistency_and_symmetry(cuda):
         assert r.converged
         path = cn.simulate(sp, cn.fit_policy(cn.build_state_grid(sp), r.policy), np.zeros(sp.J), 10_000)
         np.testing.assert_allclose(path.controls[:, i], path.controls[:, j], atol=1e-6)
+
+
+def test_acceptance_plan_invariance_512_nodes(cuda):
+    """T/test_acceptance.py #8: example3 at degree 7 (512 nodes), plans 1/8/64/256 blocks and 1/2
+    workers give bitwise-identical values, policies and histories."""
+    spec = cn.preset_spec("example3", Np=7, Nu=7, h=1e-2, tol=1e-3, max_iters=20_000)
+    n = int(np.prod(spec.Np + 1))
+    assert n == 512
+    base = quiet(cn.solve, spec, plan=cn.partition(n, 1), workers=1)
+    assert base.converged
+    for nb, workers in ((8, 1), (64, 1), (256, 1), (8, 2), (64, 2)):
+        other = quiet(cn.solve, spec, plan=cn.partition(n, nb), workers=workers)
+        assert other.converged and other.iterations == base.iterations
+        assert np.array_equal(other.values.values, base.values.values)
+        assert np.array_equal(other.policy.values, base.policy.values)
+        assert np.array_equal(other.history, base.history)
