@@ -666,6 +666,12 @@ def run_ours(args):
         roofline = {"bound": "hbm", "kernel": "eval_grid (K3 mode products)", "achieved": achieved,
                     "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                     "algorithmic": "8*(n^J + k^J) bytes per step", "traffic": ncu_traffic("eval_grid", cfg)}
+        # e2e warm-up: the first two calls allocate the pinned 1.95 GB result buffers (torch's
+        # caching host allocator reuses them afterwards)
+        res = None
+        for _ in range(max(2, args.warmup)):
+            res = cn.eval_grid(cn.tensor_coeffs(w.values, bases), targets)
+        barrier(world)
         t0 = time.perf_counter()
         for _ in range(args.steps):
             res = cn.eval_grid(cn.tensor_coeffs(w.values, bases), targets)
