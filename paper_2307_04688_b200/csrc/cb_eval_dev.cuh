@@ -161,6 +161,12 @@ __device__ __forceinline__ void consumer_sync_n(int nthreads) {
 }
 
 
+// Row-contraction evaluator shape: 16 consumer warps + producer + builder + finisher, stages of
+// kRcRows coefficient rows.
+constexpr int kRcConsumers = 16;
+constexpr int kRcThreads = (kRcConsumers + 3) * 32;
+constexpr int kRcRows = 128;
+
 // Row-contraction evaluator launch (cb_eval_rc.cu): NL leading modes, MTK DMMA m-tiles over k,
 // KT exact DFMA tail columns (-1: runtime p.ktail).  Returns false if not instantiated.
 bool launch_eval_rc(int NL, int MTK, int KT, unsigned grid, size_t bytes, cudaStream_t stream, const EvalParams& p,

@@ -19,10 +19,10 @@ namespace {
 // only once per tile (no per-stage epilogue / DMMA drain).
 // ------------------------------------------------------------------------------------------
 template <int NL, int MTK, int KT>
-__global__ void __launch_bounds__(Roles<16>::THREADS, 1)
+__global__ void __launch_bounds__(kRcThreads, 1)
     eval_rc_kernel(const __grid_constant__ EvalParams p, const __grid_constant__ DmmaSmem sm,
                    const __grid_constant__ CUtensorMap amap) {
-  constexpr int NCW = 16, NT = 2, kRows = 64;
+  constexpr int NCW = kRcConsumers, NT = 2, kRows = kRcRows, KS = kRows / 16;  // KS k-steps per warp per stage
   constexpr int J = NL + 1;
   constexpr int KTMAX = (KT < 0) ? 3 : KT;        // DFMA tail columns (compile-time when KT >= 0)
   const int ktail = (KT < 0) ? p.ktail : KT;
@@ -31,6 +31,8 @@ __global__ void __launch_bounds__(Roles<16>::THREADS, 1)
   uint64_t* bar_empty = bar_full + kMaxStages;
   uint64_t* tab_full = bar_empty + kMaxStages;
   uint64_t* tab_empty = tab_full + 2;
+  uint64_t* red_full = tab_empty + 2;   // [2] per-warp tile partials written (NCW arrivals)
+  uint64_t* red_empty = red_full + 2;   // [2] partials consumed by the finisher
   double* Src = reinterpret_cast<double*>(smem_raw + sm.src);        // [ntab][P]
   double* Red = reinterpret_cast<double*>(smem_raw + sm.red);        // [2][4][P]
   double* Ts = reinterpret_cast<double*>(smem_raw + sm.ts);          // [ntab][ts_stride]
@@ -46,7 +48,9 @@ __global__ void __launch_bounds__(Roles<16>::THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tab_full[s], 1);
-      mbar_init(&tab_empty[s], NCW);
+      mbar_init(&tab_empty[s], NCW + 1);  // consumers + finisher (reads Src)
+      mbar_init(&red_full[s], NCW);
+      mbar_init(&red_empty[s], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -102,7 +106,31 @@ __global__ void __launch_bounds__(Roles<16>::THREADS, 1)
     return;
   }
 
-  // consumers: warp = (row group rg: 16 rows of each stage) x (point group ng: 16 points)
+  if (warp == NCW + 2) {  // finisher: sums the warps' tile partials and writes the results
+    int it = 0;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int ts = it % sm.ntab;
+      const int rb = it & 1;
+      mbar_wait(&red_full[rb], (it >> 1) & 1);
+      const double* Rb = Red + rb * 8 * kP;
+      for (int pp = lane; pp < kP; pp += 32) {
+        const long long g = tile * kP + pp;
+        if (g < p.M) {
+          double v = ((Rb[pp] + Rb[kP + pp]) + Rb[2 * kP + pp]) + Rb[3 * kP + pp];
+          if (KTMAX > 0 && ktail) v += ((Rb[4 * kP + pp] + Rb[5 * kP + pp]) + Rb[6 * kP + pp]) + Rb[7 * kP + pp];
+          p.out[g] = v - Src[ts * kP + pp];
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&red_empty[rb]);
+        mbar_arrive(&tab_empty[ts]);
+      }
+    }
+    return;
+  }
+
+  // consumers: warp = (row group rg: kRows/4 rows of each stage) x (point group ng: 16 points)
   const int rg = warp >> 2, ng = warp & 3;
   const int gq = lane >> 2, tq = lane & 3;
   const int pcol = ng * 16 + gq;  // B-fragment column (point) of this lane (+ nt*8)
@@ -126,8 +154,8 @@ __global__ void __launch_bounds__(Roles<16>::THREADS, 1)
 
     for (int blk = 0; blk < p.nstage_blocks; ++blk) {
       mbar_wait(&bar_full[slot], phase);
-      const double* Ast = As + static_cast<size_t>(slot) * kRows * p.kc + (rg * 16 + tq) * p.kc + gq;
-      const int rbase = blk * kRows + rg * 16 + tq;   // this lane's row at k-step ks: rbase + 4*ks
+      const double* Ast = As + static_cast<size_t>(slot) * kRows * p.kc + (rg * (kRows / 4) + tq) * p.kc + gq;
+      const int rbase = blk * kRows + rg * (kRows / 4) + tq;   // this lane's row at k-step ks: rbase + 4*ks
       // one k-step: 4 rows of the stage; the row digits come straight from FastDiv (no carries),
       // so the fully-valid case below is straight-line code the scheduler can software-pipeline
       // B fragments W[r][p] of k-step ks for this lane's row r and points pcol + 8*nt (zero past R)
@@ -158,10 +186,15 @@ __global__ void __launch_bounds__(Roles<16>::THREADS, 1)
         double a[MTK];
 #pragma unroll
         for (int m = 0; m < MTK; ++m) a[m] = Ast[ks * 4 * p.kc + m * 8];
+        // issue order: no two consecutive DMMAs share an A or B register (a shared operand in
+        // back-to-back DMMAs costs the warp an issue bubble)
 #pragma unroll
-        for (int m = 0; m < MTK; ++m)
+        for (int h = 0; h < NT; ++h)
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) dmma884(acc[m][nt][0], acc[m][nt][1], a[m], w[nt]);
+          for (int m = 0; m < MTK; ++m) {
+            const int nt = (m + h) % NT;
+            dmma884(acc[m][nt][0], acc[m][nt][1], a[m], w[nt]);
+          }
         // tail columns k = 8*MTK + t (t < ktail) on DFMA: lane-partial sums over its rows
 #pragma unroll
         for (int t = 0; t < KTMAX; ++t) {
@@ -172,15 +205,15 @@ __global__ void __launch_bounds__(Roles<16>::THREADS, 1)
           }
         }
       };
-      const int kvalid = min(4, (static_cast<int>(p.R8) - (blk * kRows + rg * 16) + 3) / 4);  // k-steps with rows < R8
-      if (kvalid == 4) {
+      const int kvalid = min(KS, (static_cast<int>(p.R8) - (blk * kRows + rg * (kRows / 4)) + 3) / 4);  // k-steps with rows < R8
+      if (kvalid == KS) {
         // software-pipelined: the next k-step's W products are formed (and pinned in program
         // order by the volatile asm) before this k-step's DMMAs, hiding the DMUL latency
         double wc[NT], wn[NT];
         wfrag(0, wc);
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-          if (ks + 1 < 4) {
+        for (int ks = 0; ks < KS; ++ks) {
+          if (ks + 1 < KS) {
             wfrag(ks + 1, wn);
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) asm volatile("" : "+d"(wn[nt]));
@@ -233,7 +266,10 @@ __global__ void __launch_bounds__(Roles<16>::THREADS, 1)
         }
       }
     }
-    double* Rb = Red + (it & 1) * 8 * kP;  // [2][rg: 4 main + 4 tail][P]
+    // hand the tile's partials to the finisher warp (no consumer-wide barrier at the tile end)
+    const int rb = it & 1;
+    if (it >= 2) mbar_wait(&red_empty[rb], ((it >> 1) & 1) ^ 1);
+    double* Rb = Red + rb * 8 * kP;  // [2][rg: 4 main + 4 tail][P]
     if (gq == 0) {
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
@@ -244,17 +280,11 @@ __global__ void __launch_bounds__(Roles<16>::THREADS, 1)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) Rb[(4 + rg) * kP + pcol + nt * 8] = tv[nt];
     }
-    consumer_sync_n(NCW * 32);
-    if (tid < kP) {
-      const long long g = tile * kP + tid;
-      if (g < p.M) {
-        double v = ((Rb[tid] + Rb[kP + tid]) + Rb[2 * kP + tid]) + Rb[3 * kP + tid];
-        if (KTMAX > 0 && ktail) v += ((Rb[4 * kP + tid] + Rb[5 * kP + tid]) + Rb[6 * kP + tid]) + Rb[7 * kP + tid];
-        p.out[g] = v - Src[ts * kP + tid];
-      }
-    }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&tab_empty[ts]);
+    if (lane == 0) {
+      mbar_arrive(&red_full[rb]);
+      mbar_arrive(&tab_empty[ts]);
+    }
   }
 }
 
@@ -268,7 +298,7 @@ bool launch_eval_rc(int NL, int MTK, int KT, unsigned grid, size_t bytes, cudaSt
 #define CB_RC(v, m, t)                                                                                    \
   case (v * 8 + m) * 8 + (t + 1):                                                                         \
     ensure_smem_attr(reinterpret_cast<const void*>(eval_rc_kernel<v, m, t>), 227 * 1024);                 \
-    eval_rc_kernel<v, m, t><<<grid, Roles<16>::THREADS, bytes, stream>>>(p, sm, amap);                    \
+    eval_rc_kernel<v, m, t><<<grid, kRcThreads, bytes, stream>>>(p, sm, amap);                    \
     return true;
 #define CB_RCT(v, m) CB_RC(v, m, 0) CB_RC(v, m, 1) CB_RC(v, m, 2) CB_RC(v, m, 3)
 #define CB_RCM(v, X) X(v, 1) X(v, 2) X(v, 3) X(v, 4) X(v, 5) X(v, 6)
