@@ -107,6 +107,24 @@ int cb_eval_advected(int J, const int64_t* n, const double* d_coef, int64_t node
                      const double* A, double dt, const double* lo, const double* hi, int source, double* d_out,
                      void* stream);
 
+/* K4 with the exchange fused in (node-sharded loop across GPUs): as
+ * cb_eval_advected, but every result V(y_i) is stored into ALL G buffers d_full[r][i] (each the
+ * base of one rank's full node-value array, peers mapped over NVLink with cb_ipc_import), so the
+ * evaluation kernel itself performs the per-step all-gather.  Replaces the slab evaluation +
+ * NCCL all-gather of dist.ShardedAdvectLoop (the reference's block sweep S/solver.py:412-438
+ * with its barrier before _refit :441-449).  d_full: host array of G <= 8 device pointers. */
+int cb_eval_advected_peers(int J, const int64_t* n, const double* d_coef, int64_t node_begin, int64_t count,
+                           const double* A, double dt, const double* lo, const double* hi, int source,
+                           double* const* d_full, int G, void* stream);
+
+/* CUDA IPC for the peer buffers of cb_eval_advected_peers.  cb_ipc_export writes a 72-byte
+ * record (cudaIpcMemHandle_t of the allocation holding d_ptr + the byte offset of d_ptr in it);
+ * cb_ipc_import maps a record exported by another process (same node) and returns the peer's
+ * pointer and the mapping base to pass to cb_ipc_close. */
+int cb_ipc_export(const void* d_ptr, void* record72);
+int cb_ipc_import(const void* record72, void** d_ptr_out, void** d_base_out);
+int cb_ipc_close(void* d_base);
+
 /* K4 — device-resident time loop on one GPU (solver.py:541-550 skeleton, BASELINE configs 3/5b):
  *   repeat `steps` times:  C = tensor_coeffs(V);  V <- eval_advected(C) (source on).
  * d_values: dense (n_1..n_J) V_0 in, V_steps out.  d_tmp: same size scratch.  d_coef: eval-layout

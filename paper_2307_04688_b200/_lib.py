@@ -67,6 +67,12 @@ SIGNATURES = {
     "cb_eval_points": (_c_int, [_c_int, _i64p, _vp, _c_i64, _vp, _vp, _vp, _c_int, _vp]),
     "cb_eval_points_host": (_c_int, [_c_int, _i64p, _vp, _c_i64, _vp, _vp, _vp, _vp, _vp, _c_int, _vp]),
     "cb_eval_advected": (_c_int, [_c_int, _i64p, _vp, _c_i64, _c_i64, _dblp, _c_dbl, _dblp, _dblp, _c_int, _vp, _vp]),
+    "cb_eval_advected_peers": (
+        _c_int, [_c_int, _i64p, _vp, _c_i64, _c_i64, _dblp, _c_dbl, _dblp, _dblp, _c_int, ctypes.POINTER(_vp), _c_int, _vp]
+    ),
+    "cb_ipc_export": (_c_int, [_vp, _vp]),
+    "cb_ipc_import": (_c_int, [_vp, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
+    "cb_ipc_close": (_c_int, [_vp]),
     "cb_advect_loop": (_c_int, [_c_int, _i64p, _vp, _vp, _vp, _c_int, _dblp, _c_dbl, _dblp, _dblp, _vp, _c_int, _vp]),
     "cb_contract_axis": (_c_int, [_c_i64, _c_int, _c_i64, _c_i64, _c_int, _vp, _vp, _vp, _c_i64, _c_i64, _c_i64, _vp]),
     "cb_contract_diagonal": (

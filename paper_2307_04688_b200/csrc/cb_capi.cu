@@ -6,6 +6,7 @@
 #include <atomic>
 #include <mutex>
 #include <string>
+#include <cuda.h>
 #include "../../include/chebnash_b200.h"
 #include "cb_common.cuh"
 #include "cb_kernels.h"
@@ -324,6 +325,78 @@ int cb_eval_advected(int J, const int64_t* n, const double* d_coef, int64_t node
   adv.node_begin = node_begin;
   CB_CUDA(eval_points(L, d_coef, count, nullptr, &adv, d_out, nullptr, 0, static_cast<cudaStream_t>(stream)),
           "cb_eval_advected");
+  return CB_OK;
+}
+
+int cb_eval_advected_peers(int J, const int64_t* n, const double* d_coef, int64_t node_begin, int64_t count,
+                           const double* A, double dt, const double* lo, const double* hi, int source,
+                           double* const* d_full, int G, void* stream) {
+  int rc = check_dims(J, n, "cb_eval_advected_peers");
+  if (rc) return rc;
+  for (int d = 0; d < J; ++d)
+    if (n[d] > 64) return fail(CB_EINVAL, "cb_eval_advected_peers: mode size above 64 not supported");
+  if (G < 1 || G > 8 || !d_full) return fail(CB_EINVAL, "cb_eval_advected_peers: need 1..8 destination buffers");
+  for (int r = 0; r < G; ++r)
+    if (!d_full[r]) return fail(CB_EINVAL, "cb_eval_advected_peers: null destination buffer");
+  EvalLayout L = layout_of(J, n);
+  AdvectSpec adv;
+  rc = fill_advect(J, A, dt, lo, hi, source, adv);
+  if (rc) return rc;
+  adv.node_begin = node_begin;
+  adv.npeers = G;
+  for (int r = 0; r < G; ++r) adv.peers[r] = d_full[r];
+  CB_CUDA(eval_points(L, d_coef, count, nullptr, &adv, d_full[0] + node_begin, nullptr, 0,
+                      static_cast<cudaStream_t>(stream)),
+          "cb_eval_advected_peers");
+  return CB_OK;
+}
+
+// cuMemGetAddressRange through the runtime's driver entry point (the library links no libcuda)
+typedef CUresult (*PFN_getAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+static PFN_getAddressRange address_range_fn() {
+  static PFN_getAddressRange fn = [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      ptr = nullptr;
+    return reinterpret_cast<PFN_getAddressRange>(ptr);
+  }();
+  return fn;
+}
+
+int cb_ipc_export(const void* d_ptr, void* record72) {
+  if (!d_ptr || !record72) return fail(CB_EINVAL, "cb_ipc_export: null pointer");
+  PFN_getAddressRange range = address_range_fn();
+  if (!range) return fail(CB_ECUDA, "cb_ipc_export: cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(d_ptr)) != CUDA_SUCCESS)
+    return fail(CB_ECUDA, "cb_ipc_export: pointer is not device memory");
+  cudaIpcMemHandle_t h;
+  CB_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)), "cb_ipc_export");
+  const uint64_t off = static_cast<uint64_t>(reinterpret_cast<CUdeviceptr>(d_ptr) - base);
+  std::memcpy(record72, &h, 64);
+  std::memcpy(static_cast<char*>(record72) + 64, &off, 8);
+  return CB_OK;
+}
+
+int cb_ipc_import(const void* record72, void** d_ptr_out, void** d_base_out) {
+  if (!record72 || !d_ptr_out || !d_base_out) return fail(CB_EINVAL, "cb_ipc_import: null pointer");
+  cudaIpcMemHandle_t h;
+  uint64_t off = 0;
+  std::memcpy(&h, record72, 64);
+  std::memcpy(&off, static_cast<const char*>(record72) + 64, 8);
+  void* base = nullptr;
+  CB_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess), "cb_ipc_import");
+  *d_base_out = base;
+  *d_ptr_out = static_cast<char*>(base) + off;
+  return CB_OK;
+}
+
+int cb_ipc_close(void* d_base) {
+  if (!d_base) return CB_OK;
+  CB_CUDA(cudaIpcCloseMemHandle(d_base), "cb_ipc_close");
   return CB_OK;
 }
 

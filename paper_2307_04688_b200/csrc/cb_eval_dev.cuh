@@ -13,6 +13,7 @@ constexpr int kBP = kP + 4;            // smem pitch of the B table (bank-confli
 constexpr int kTP = kP + 4;            // smem pitch of the per-dim T tables (8 rows per warp lookup)
 constexpr int kMaxStages = 4;
 constexpr int kMaxNodeTab = 64;        // nodes per dim carried in the kernel params (advection)
+constexpr int kMaxPeers = 8;           // GPUs one evaluation can store its results into
 
 struct EvalParams {
   const double* coef;   // eval layout [R8][Kp]
@@ -40,7 +41,22 @@ struct EvalParams {
   double lo[kMaxDims], hi[kMaxDims];
   int source;
   double nodes[kMaxDims][kMaxNodeTab];
+  // fused exchange (multi-GPU loop): results go to every rank's node-value buffer through
+  // NVLink peer stores instead of `out` (peers[r] already offset to this launch's first node)
+  int npeers;
+  double* peers[kMaxPeers];
 };
+
+// Result store of every evaluator: `out`, or all peers' buffers (the all-gather fused into the
+// evaluation: each rank writes its slab straight into every rank's copy of the node values).
+__device__ __forceinline__ void emit(const EvalParams& p, long long g, double v) {
+  if (p.npeers == 0) {
+    p.out[g] = v;
+    return;
+  }
+#pragma unroll 1
+  for (int r = 0; r < p.npeers; ++r) p.peers[r][g] = v;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

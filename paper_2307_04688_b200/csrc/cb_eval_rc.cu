@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(kRcThreads, 1)
         if (g < p.M) {
           double v = ((Rb[pp] + Rb[kP + pp]) + Rb[2 * kP + pp]) + Rb[3 * kP + pp];
           if (KTMAX > 0 && ktail) v += ((Rb[4 * kP + pp] + Rb[5 * kP + pp]) + Rb[6 * kP + pp]) + Rb[7 * kP + pp];
-          p.out[g] = v - Src[ts * kP + pp];
+          emit(p, g, v - Src[ts * kP + pp]);
         }
       }
       __syncwarp();

@@ -40,6 +40,8 @@ struct AdvectSpec {
   double dt;
   double lo[kMaxDims], hi[kMaxDims];  // state box per dim (the grid basis interval)
   int source;               // subtract dt*|x|^2 of the (unclipped) node
+  int npeers;               // > 0: store results into peers[r][node] (full node-value buffers) instead of out
+  double* peers[8];
 };
 const char* last_eval_plan();  // kernel / plan chosen by the last eval_points on this thread
 cudaError_t eval_points(const EvalLayout& L, const double* coef, long long M, const double* points,

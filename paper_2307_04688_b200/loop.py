@@ -12,6 +12,8 @@ contiguous slabs and the node values are all-gathered once per step (dist.py).
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 
 from . import _lib
@@ -94,3 +96,64 @@ class CudaStepBackend:
     def finish(self, full_values):
         _lib.raise_for_samples(self.status)
         return full_values
+
+    # --- fused exchange (dist.PeerShardedAdvectLoop) ---
+    def exchange_buffers(self, bufs, group=None):
+        """CUDA-IPC map every rank's node-value buffers: returns dests[b][r] = device address of
+        rank r's buffer b in this process (own buffers unmapped)."""
+        import torch.distributed as dist
+
+        lib = _lib.load()
+        self._mapped = []
+        recs = []
+        for b in bufs:
+            rec = ctypes.create_string_buffer(72)
+            _lib.check(lib.cb_ipc_export(_lib.ptr(b), rec), "ipc_export")
+            recs.append(rec.raw)
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        allrecs = [recs]
+        if world > 1:
+            allrecs = [None] * world
+            dist.all_gather_object(allrecs, recs, group=group)
+        dests = [[0] * world for _ in bufs]
+        for r in range(world):
+            for i, b in enumerate(bufs):
+                if r == rank:
+                    dests[i][r] = _lib.ptr(b)
+                    continue
+                p, base = ctypes.c_void_p(), ctypes.c_void_p()
+                _lib.check(lib.cb_ipc_import(allrecs[r][i], ctypes.byref(p), ctypes.byref(base)), "ipc_import")
+                self._mapped.append(base.value)
+                dests[i][r] = p.value
+        t = _lib.require_cuda()
+        self._flag = t.zeros(1, dtype=t.float64, device=_lib.device())
+        return dests
+
+    def eval_slab_peers(self, begin: int, count: int, dests):
+        if count <= 0:
+            return
+        arr = (ctypes.c_void_p * len(dests))(*dests)
+        _lib.check(_lib.load().cb_eval_advected_peers(self.J, self.sizes, _lib.ptr(self.coef), int(begin), int(count),
+                                                      self.A, self.dt, self.lo, self.hi, 1, arr, len(dests),
+                                                      _lib.stream_handle()),
+                   "eval_slab_peers")
+
+    def barrier(self, group=None):
+        """Orders every rank's peer stores of this step before any rank's next build: a 1-element
+        NCCL all-reduce on the compute stream (host-asynchronous); under gloo (several ranks sharing
+        one GPU in the tests) a device synchronize + host barrier."""
+        import torch.distributed as dist
+
+        if not dist.is_initialized() or dist.get_world_size(group) == 1:
+            return
+        if dist.get_backend(group) == "nccl":
+            dist.all_reduce(self._flag, group=group)
+        else:
+            _lib.require_cuda().cuda.synchronize()
+            dist.barrier(group=group)
+
+    def close_buffers(self):
+        for base in getattr(self, "_mapped", []):
+            _lib.load().cb_ipc_close(base)
+        self._mapped = []

@@ -104,3 +104,84 @@ def test_shard_range_covers_exactly():
             assert sum(e - b for b, e, _ in pieces) == total
     with pytest.raises(ValueError):
         shard_range(10, 2, 2)
+
+
+# ------------------------------------------------------------------------------------------------
+# Fused exchange (PeerShardedAdvectLoop): every rank stores its slab into all ranks' buffers.
+# Here the "peer memory" is shared CPU tensors (torch shared memory) standing in for CUDA IPC
+# mappings; the ping-pong / barrier protocol under test is the product's.
+# ------------------------------------------------------------------------------------------------
+
+class SharedPeerBackend(HostBackend):
+    def __init__(self, shape, A, dt, shared, rank):
+        super().__init__(shape, A, dt)
+        self.shared = shared    # shared[r][b]: rank r's buffer b (shared memory)
+        self.rank = rank
+        self.nz = 0
+
+    def zeros(self, n):
+        t = self.shared[self.rank][self.nz]
+        self.nz += 1
+        t.zero_()
+        return t
+
+    def exchange_buffers(self, bufs, group=None):
+        world = len(self.shared)
+        return [[self.shared[r][b] for r in range(world)] for b in range(len(bufs))]
+
+    def eval_slab_peers(self, begin, count, dests):
+        if count <= 0:
+            return
+        v = torch.from_numpy(self.orc.eval_points(self.C, self.T[begin:begin + count]) - self.S[begin:begin + count])
+        for d in dests:
+            d[begin:begin + count].copy_(v)
+
+    def barrier(self, group=None):
+        dist.barrier(group=group)
+
+    def close_buffers(self):
+        pass
+
+
+def _peer_worker(rank, world, port, shape, A, V0, steps, shared, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2307_04688_b200.dist import PeerShardedAdvectLoop
+
+        loop = PeerShardedAdvectLoop(shape, SharedPeerBackend(shape, A, 0.01, shared, rank))
+        V1 = loop.run(V0, steps)
+        V2 = loop.run(V0, steps + 1)   # a second run on the same buffers (other parity)
+        q.put((rank, V1.numpy().copy(), V2.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("shape,world", [((5, 5, 5), 2), ((4, 3, 5), 3)])
+def test_peer_loop_matches_single(shape, world):
+    from oracle import cheb_oracle as orc
+
+    rng = np.random.default_rng(11)
+    J = len(shape)
+    A = rng.uniform(-0.5, 0.5, (J, J))
+    V0 = rng.standard_normal(shape)
+    N = int(np.prod(shape))
+    shared = [[torch.zeros(N, dtype=torch.float64).share_memory_() for _ in range(2)] for _ in range(world)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, shape, A, V0, 3, shared, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in procs:
+        r, v1, v2 = q.get(timeout=120)
+        res[r] = (v1, v2)
+    for p in procs:
+        p.join(timeout=60)
+    ref1 = orc.advect_loop(V0, A, 0.01, 3)
+    ref2 = orc.advect_loop(V0, A, 0.01, 4)
+    for r in range(world):
+        assert np.array_equal(res[r][0], ref1), (r, np.abs(res[r][0] - ref1).max())
+        assert np.array_equal(res[r][1], ref2), (r, np.abs(res[r][1] - ref2).max())
