@@ -14,7 +14,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libchebnash_b200.so")
+# CHEBNASH_B200_LIB: load another build of the same library (tools/ experiments only)
+LIB_PATH = os.environ.get("CHEBNASH_B200_LIB") or os.path.join(_HERE, "libchebnash_b200.so")
 
 _c_int = ctypes.c_int
 _c_i64 = ctypes.c_int64

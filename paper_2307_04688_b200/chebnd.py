@@ -334,13 +334,24 @@ def tensor_coeffs(samples, bases) -> CoefTensor:
     s_shape = tuple(samples.shape) if _is_tensor(samples) else np.shape(samples)
     if tuple(s_shape) != shape:
         raise ValueError(f"sample shape {tuple(s_shape)} does not match bases {shape}")
-    ds = _lib.to_device(samples if _is_tensor(samples) else np.asarray(samples, dtype=float))
+    if _is_tensor(samples) and samples.is_cuda:
+        ds = samples
+        st = _lib.new_status()  # device data: the build's status block reports non-finite samples
+    else:
+        # host data (numpy / CPU tensor): validated here (S/chebnd.py:181-185), so the build is
+        # enqueued without a device status read-back — no host synchronisation in this call
+        host = samples.detach().numpy() if _is_tensor(samples) else np.asarray(samples, dtype=float)
+        if not np.isfinite(host).all():
+            raise ValueError("samples must be finite")
+        ds = samples if _is_tensor(samples) else host
+        st = None
+    ds = _lib.to_device(ds)
     L = _lib.eval_layout(shape)
     out = _lib.empty((L["elems"],))
-    st = _lib.new_status()
     _lib.check(_lib.load().cb_tensor_coeffs(len(shape), _lib.i64_array(shape), _lib.ptr(ds), _lib.ptr(out),
                                             _lib.ptr(st), _lib.stream_handle()), "tensor_coeffs")
-    _lib.raise_for_samples(st)
+    if st is not None:
+        _lib.raise_for_samples(st)
     return CoefTensor._from_eval_layout(bases, out)
 
 
@@ -425,9 +436,14 @@ def _eval_points_pinned(tensor: CoefTensor, points, check: bool):
                                                _lib.ptr(tensor.device_coefficients), M, points.data_ptr(),
                                                host_out.data_ptr(), _lib.ptr(ws_pts), _lib.ptr(ws_out), _lib.ptr(st),
                                                0, _lib.stream_handle()), "eval_points")
+    host_st = None
+    if check:
+        # the status block rides back behind the results: one synchronisation per call
+        host_st = t.empty((2,), dtype=t.int64, pin_memory=True)
+        host_st.copy_(st, non_blocking=True)
     t.cuda.current_stream().synchronize()
     if check:
-        _lib.raise_for_points(st)
+        _lib.raise_for_points(host_st)
     return host_out
 
 

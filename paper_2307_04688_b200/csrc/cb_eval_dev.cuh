@@ -11,7 +11,10 @@ namespace evk {
 constexpr int kP = 64;                 // points per CTA
 constexpr int kBP = kP + 4;            // smem pitch of the B table (bank-conflict free fragments)
 constexpr int kTP = kP + 4;            // smem pitch of the per-dim T tables (8 rows per warp lookup)
-constexpr int kMaxStages = 4;
+#ifndef CB_MAX_STAGES
+#define CB_MAX_STAGES 4
+#endif
+constexpr int kMaxStages = CB_MAX_STAGES;
 constexpr int kMaxNodeTab = 64;        // nodes per dim carried in the kernel params (advection)
 constexpr int kMaxPeers = 8;           // GPUs one evaluation can store its results into
 
@@ -181,7 +184,10 @@ __device__ __forceinline__ void consumer_sync_n(int nthreads) {
 // kRcRows coefficient rows.
 constexpr int kRcConsumers = 16;
 constexpr int kRcThreads = (kRcConsumers + 3) * 32;
-constexpr int kRcRows = 128;
+#ifndef CB_RC_ROWS
+#define CB_RC_ROWS 128
+#endif
+constexpr int kRcRows = CB_RC_ROWS;
 
 // Row-contraction evaluator launch (cb_eval_rc.cu): NL leading modes, MTK DMMA m-tiles over k,
 // KT exact DFMA tail columns (-1: runtime p.ktail).  Returns false if not instantiated.
