@@ -172,6 +172,14 @@ int64_t cb_eval_grid_workspace(int J, const int64_t* n, const int64_t* k);
 int cb_eval_grid(int J, const int64_t* n, const double* d_coef, const int64_t* k, const double* const* d_E,
                  double* d_out, double* d_work, int64_t work_elems, void* stream);
 
+/* cb_eval_grid from the target coordinates (eval_axis's basis_matrix step included, chebnd.py:
+ * 224-233): d_targets[j] holds k_j reference coordinates of dim j (clamp_reference, errors into
+ * d_status); all J evaluation matrices are formed in ONE launch into d_E_ws (sum_j k_j*n_j
+ * doubles, matrix j at offset sum_{i<j} k_i*n_i), then the mode-product passes run. */
+int cb_eval_grid_targets(int J, const int64_t* n, const double* d_coef, const int64_t* k,
+                         const double* const* d_targets, double* d_E_ws, void* d_status, double* d_out,
+                         double* d_work, int64_t work_elems, void* stream);
+
 /* ---------------------------------------------------------------------------------------------
  * Collocation solver: the Bellman sweep of solver.py on the device.
  * ------------------------------------------------------------------------------------------- */

@@ -86,6 +86,8 @@ SIGNATURES = {
     "cb_gather_take": (_c_int, [_c_int, _i64p, _vp, _c_i64, _vp, _c_int, _i64p, _vp, _vp]),
     "cb_eval_grid_workspace": (_c_i64, [_c_int, _i64p, _i64p]),
     "cb_eval_grid": (_c_int, [_c_int, _i64p, _vp, _i64p, ctypes.POINTER(_vp), _vp, _vp, _c_i64, _vp]),
+    "cb_eval_grid_targets": (_c_int, [_c_int, _i64p, _vp, _i64p, ctypes.POINTER(_vp), _vp, _vp, _vp, _vp, _c_i64,
+                                      _vp]),
     "cb_solver_drift_elems": (_c_i64, [_gamep]),
     "cb_solver_drift_layout": (_c_int, [_gamep, _vp, _vp, _vp]),
     "cb_bellman_sweep": (_c_int, [_gamep, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),

@@ -540,22 +540,19 @@ def _eval_grid_device(shape, coef_dev, targets_dev, status=None, work=None, out=
     coefficients + per-dim CUDA target vectors -> CUDA (k_1, ..., k_J)."""
     J = len(shape)
     ks = [int(tv.shape[0]) for tv in targets_dev]
-    # all J evaluation matrices in one allocation (the C side reads them stream-ordered)
+    # one C call: the J evaluation matrices (one launch, into one allocation) + the mode passes
     Eall = _lib.empty((sum(k * n for k, n in zip(ks, shape)),))
-    Es, off = [], 0
-    for j, tv in enumerate(targets_dev):
-        view = Eall[off:off + ks[j] * shape[j]].view(ks[j], shape[j])
-        Es.append(_basis_device(tv, shape[j], True, status, out=view))
-        off += ks[j] * shape[j]
     lib = _lib.load()
     work_elems = int(lib.cb_eval_grid_workspace(J, _lib.i64_array(shape), _lib.i64_array(ks)))
     if work is None or work.numel() < max(1, work_elems):
         work = _lib.empty((max(1, work_elems),))
     if out is None:
         out = _lib.empty(tuple(ks))
-    eptrs = (ctypes.c_void_p * J)(*[_lib.ptr(e) for e in Es])
-    _lib.check(lib.cb_eval_grid(J, _lib.i64_array(shape), _lib.ptr(coef_dev), _lib.i64_array(ks), eptrs,
-                                _lib.ptr(out), _lib.ptr(work), work_elems, _lib.stream_handle()), "eval_grid")
+    tv = [tv if tv.dtype == _lib.torch().float64 and tv.is_contiguous() else _lib.to_device(tv) for tv in targets_dev]
+    tptrs = (ctypes.c_void_p * J)(*[_lib.ptr(t) for t in tv])
+    _lib.check(lib.cb_eval_grid_targets(J, _lib.i64_array(shape), _lib.ptr(coef_dev), _lib.i64_array(ks), tptrs,
+                                        _lib.ptr(Eall), _lib.ptr(status), _lib.ptr(out), _lib.ptr(work), work_elems,
+                                        _lib.stream_handle()), "eval_grid")
     return out
 
 

@@ -168,6 +168,29 @@ __global__ void basis_matrix_kernel(long long k, const double* x, int size, doub
   }
 }
 
+// All J evaluation matrices of a structured evaluation in one launch: thread per target point
+// (dim d found from the prefix sums), row j of E_d = T_0..T_{n_d - 1}(clamp_reference(t_{d,j})).
+struct BasisBatch {
+  const double* x[kMaxDims];
+  double* out[kMaxDims];
+  long long kcum[kMaxDims + 1];
+  int size[kMaxDims];
+  int J;
+  Status* st;
+};
+
+__global__ void basis_batch_kernel(const __grid_constant__ BasisBatch p) {
+  const long long total = p.kcum[p.J];
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    int d = 0;
+    while (d + 1 < p.J && i >= p.kcum[d + 1]) ++d;
+    const long long j = i - p.kcum[d];
+    const double v = clamp_ref(__ldg(p.x[d] + j), p.st);
+    cheb_row(v, p.size[d], p.out[d] + j * p.size[d], 1);
+  }
+}
+
 __global__ void gather_index_kernel(long long rest, long long count, long long* flat) {
   const long long total = rest * count;
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
@@ -233,10 +256,12 @@ __global__ void derivative_kernel(long long rows, int L, const double* in, doubl
 // stream-ordered device-to-device copy right before the kernel that reads them (no host sync);
 // every DFMA then takes its matrix entry as a constant-bank operand.  Calls on different streams
 // are ordered through ConstSlotGuard (eval_grid).
-constexpr int kCESlot = 1024;
-__constant__ double cGridE[2][kCESlot];
+// Mode d's (K x N) matrix sits at offset d*K*N: a uniform grid (every mode the same (N, K)) is
+// uploaded once per call (one copy when the matrices are contiguous), other plans per pass.
+constexpr int kCETotal = 4096;
+__constant__ double cGridE[kCETotal];
 
-template <int N, int K>
+template <int N, int K, int DA>
 struct Fused2Params {
   const double* in;
   double* out;
@@ -249,36 +274,36 @@ constexpr int kF2Threads = kF2Warps * 32;
 constexpr int kF2IB = 5;       // K <= 25 (5 blocks)       // outputs per thread item (compile-time constant-bank indices)
 
 // step 1, output block B: z[ib] for ib in [B*5, B*5+5) from the N inputs v (row la, column rt)
-template <int N, int K, int B>
-__device__ __forceinline__ void f2_step1(const Fused2Params<N, K>& p, const double* v, double* z) {
+template <int N, int K, int DA, int B>
+__device__ __forceinline__ void f2_step1(const Fused2Params<N, K, DA>& p, const double* v, double* z) {
 #pragma unroll
   for (int j = 0; j < kF2IB; ++j) {
     const int ib = B * kF2IB + j;
     if (ib < K) {
       double acc = 0.0;
 #pragma unroll
-      for (int lb = 0; lb < N; ++lb) acc = fma(cGridE[1][ib * N + lb], v[lb], acc);
+      for (int lb = 0; lb < N; ++lb) acc = fma(cGridE[(DA + 1) * K * N + ib * N + lb], v[lb], acc);
       z[ib] = acc;
     }
   }
 }
 
-template <int N, int K, int B>
-__device__ __forceinline__ void f2_step2(const Fused2Params<N, K>& p, const double* v, double* dst) {
+template <int N, int K, int DA, int B>
+__device__ __forceinline__ void f2_step2(const Fused2Params<N, K, DA>& p, const double* v, double* dst) {
 #pragma unroll
   for (int j = 0; j < kF2IB; ++j) {
     const int ia = B * kF2IB + j;
     if (ia < K) {
       double acc = 0.0;
 #pragma unroll
-      for (int la = 0; la < N; ++la) acc = fma(cGridE[0][ia * N + la], v[la], acc);
+      for (int la = 0; la < N; ++la) acc = fma(cGridE[DA * K * N + ia * N + la], v[la], acc);
       dst[ia * K] = acc;
     }
   }
 }
 
-template <int N, int K>
-__global__ void __launch_bounds__(kF2Threads, 6) fused2_kernel(const __grid_constant__ Fused2Params<N, K> p) {
+template <int N, int K, int DA>
+__global__ void __launch_bounds__(kF2Threads, 6) fused2_kernel(const __grid_constant__ Fused2Params<N, K, DA> p) {
   extern __shared__ __align__(16) double f2sm[];
   double* sX = f2sm;                   // [N*N][RT]
   double* sZ = f2sm + N * N * kF2RT;   // [N][RT][K]
@@ -309,11 +334,11 @@ __global__ void __launch_bounds__(kF2Threads, 6) fused2_kernel(const __grid_cons
         for (int lb = 0; lb < N; ++lb) v[lb] = sX[(la * N + lb) * kF2RT + rt];
         double* z = sZ + (la * kF2RT + rt) * K;
         switch (blk) {
-          case 0: f2_step1<N, K, 0>(p, v, z); break;
-          case 1: if constexpr (NB > 1) f2_step1<N, K, 1>(p, v, z); break;
-          case 2: if constexpr (NB > 2) f2_step1<N, K, 2>(p, v, z); break;
-          case 3: if constexpr (NB > 3) f2_step1<N, K, 3>(p, v, z); break;
-          default: if constexpr (NB > 4) f2_step1<N, K, 4>(p, v, z); break;
+          case 0: f2_step1<N, K, DA, 0>(p, v, z); break;
+          case 1: if constexpr (NB > 1) f2_step1<N, K, DA, 1>(p, v, z); break;
+          case 2: if constexpr (NB > 2) f2_step1<N, K, DA, 2>(p, v, z); break;
+          case 3: if constexpr (NB > 3) f2_step1<N, K, DA, 3>(p, v, z); break;
+          default: if constexpr (NB > 4) f2_step1<N, K, DA, 4>(p, v, z); break;
         }
       }
     }
@@ -331,37 +356,58 @@ __global__ void __launch_bounds__(kF2Threads, 6) fused2_kernel(const __grid_cons
         for (int la = 0; la < N; ++la) v[la] = sZ[(la * kF2RT + rt) * K + ib];
         double* dst = p.out + (r0 + rt) * (K * K) + ib;
         switch (blk) {
-          case 0: f2_step2<N, K, 0>(p, v, dst); break;
-          case 1: if constexpr (NB > 1) f2_step2<N, K, 1>(p, v, dst); break;
-          case 2: if constexpr (NB > 2) f2_step2<N, K, 2>(p, v, dst); break;
-          case 3: if constexpr (NB > 3) f2_step2<N, K, 3>(p, v, dst); break;
-          default: if constexpr (NB > 4) f2_step2<N, K, 4>(p, v, dst); break;
+          case 0: f2_step2<N, K, DA, 0>(p, v, dst); break;
+          case 1: if constexpr (NB > 1) f2_step2<N, K, DA, 1>(p, v, dst); break;
+          case 2: if constexpr (NB > 2) f2_step2<N, K, DA, 2>(p, v, dst); break;
+          case 3: if constexpr (NB > 3) f2_step2<N, K, DA, 3>(p, v, dst); break;
+          default: if constexpr (NB > 4) f2_step2<N, K, DA, 4>(p, v, dst); break;
         }
       }
     }
   }
 }
 
+// Mode-d matrix into its constant offset (stream-ordered device-to-device copy).
 template <int N, int K>
-cudaError_t launch_fused2(const double* Ea, const double* Eb, const double* in, double* out, long long R,
-                          cudaStream_t stream) {
-  static_assert(K * N <= kCESlot, "constant slot too small");
-  cudaError_t e = cudaMemcpyToSymbolAsync(cGridE, Ea, sizeof(double) * K * N, 0, cudaMemcpyDeviceToDevice, stream);
-  if (e == cudaSuccess)
-    e = cudaMemcpyToSymbolAsync(cGridE, Eb, sizeof(double) * K * N, sizeof(double) * kCESlot,
-                                cudaMemcpyDeviceToDevice, stream);
+cudaError_t upload_const(int d, const double* E, cudaStream_t stream) {
+  if ((d + 1) * K * N > kCETotal) return cudaErrorInvalidValue;
+  return cudaMemcpyToSymbolAsync(cGridE, E, sizeof(double) * K * N, sizeof(double) * d * K * N,
+                                 cudaMemcpyDeviceToDevice, stream);
+}
+
+// Fused pair of modes (DA, DA+1); `uploaded`: their matrices are already in the constant bank.
+template <int N, int K, int DA>
+cudaError_t launch_fused2_at(const double* Ea, const double* Eb, bool uploaded, const double* in, double* out,
+                             long long R, cudaStream_t stream) {
+  static_assert((DA + 2) * K * N <= kCETotal, "constant bank too small");
+  cudaError_t e = cudaSuccess;
+  if (!uploaded) {
+    e = upload_const<N, K>(DA, Ea, stream);
+    if (e == cudaSuccess) e = upload_const<N, K>(DA + 1, Eb, stream);
+  }
   if (e != cudaSuccess) return e;
-  Fused2Params<N, K> p;
+  Fused2Params<N, K, DA> p;
   p.in = in;
   p.out = out;
   p.R = R;
   const long long g = (R + kF2RT - 1) / kF2RT;
   if (g > 0x7fffffffLL) return cudaErrorInvalidValue;
   const size_t smem = sizeof(double) * (N * N + N * K) * kF2RT;
-  ensure_smem_attr(reinterpret_cast<const void*>(fused2_kernel<N, K>), 200 * 1024);
-  fused2_kernel<N, K><<<static_cast<unsigned>(g), kF2Threads, smem, stream>>>(p);
+  ensure_smem_attr(reinterpret_cast<const void*>(fused2_kernel<N, K, DA>), 200 * 1024);
+  fused2_kernel<N, K, DA><<<static_cast<unsigned>(g), kF2Threads, smem, stream>>>(p);
   count_launch();
   return cudaGetLastError();
+}
+
+template <int N, int K>
+cudaError_t launch_fused2(int d, const double* Ea, const double* Eb, bool uploaded, const double* in, double* out,
+                          long long R, cudaStream_t stream) {
+  switch (d) {
+#define CB_F2(v) case v: return launch_fused2_at<N, K, v>(Ea, Eb, uploaded, in, out, R, stream);
+    CB_F2(0) CB_F2(1) CB_F2(2) CB_F2(3) CB_F2(4) CB_F2(5) CB_F2(6)
+#undef CB_F2
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 
@@ -369,7 +415,7 @@ cudaError_t launch_fused2(const double* Ea, const double* Eb, const double* in, 
 //   out[r][j] = sum_l E[j][l] in[l][r].  One row per thread, one 256-row tile per CTA (no
 //   persistent loop, so the constant operands stay in the bank), output staged in shared memory
 //   and written as one contiguous block.
-template <int N, int K>
+template <int N, int K, int D>
 struct RotParams {
   const double* in;
   double* out;
@@ -378,8 +424,8 @@ struct RotParams {
 
 constexpr int kRCThreads = 256;
 
-template <int N, int K>
-__global__ void __launch_bounds__(kRCThreads) rotate_const(const __grid_constant__ RotParams<N, K> p) {
+template <int N, int K, int D>
+__global__ void __launch_bounds__(kRCThreads) rotate_const(const __grid_constant__ RotParams<N, K, D> p) {
   extern __shared__ __align__(16) double rcs[];   // [256][K]
   const long long r0 = static_cast<long long>(blockIdx.x) * kRCThreads;
   const int rows = static_cast<int>(min(static_cast<long long>(kRCThreads), p.R - r0));
@@ -392,7 +438,7 @@ __global__ void __launch_bounds__(kRCThreads) rotate_const(const __grid_constant
     for (int j = 0; j < K; ++j) {
       double acc = 0.0;
 #pragma unroll
-      for (int l = 0; l < N; ++l) acc = fma(cGridE[0][j * N + l], v[l], acc);
+      for (int l = 0; l < N; ++l) acc = fma(cGridE[D * K * N + j * N + l], v[l], acc);
       rcs[r * K + j] = acc;
     }
   }
@@ -402,23 +448,36 @@ __global__ void __launch_bounds__(kRCThreads) rotate_const(const __grid_constant
   for (int e = threadIdx.x; e < cnt; e += blockDim.x) dst[e] = rcs[e];
 }
 
-template <int N, int K>
-cudaError_t launch_rotate_const(const double* E, const double* in, double* out, long long R,
-                                cudaStream_t stream) {
-  static_assert(K * N <= kCESlot, "constant slot too small");
-  cudaError_t e = cudaMemcpyToSymbolAsync(cGridE, E, sizeof(double) * K * N, 0, cudaMemcpyDeviceToDevice, stream);
-  if (e != cudaSuccess) return e;
-  RotParams<N, K> p;
+template <int N, int K, int D>
+cudaError_t launch_rotate_const_at(const double* E, bool uploaded, const double* in, double* out, long long R,
+                                   cudaStream_t stream) {
+  static_assert((D + 1) * K * N <= kCETotal, "constant bank too small");
+  if (!uploaded) {
+    cudaError_t e = upload_const<N, K>(D, E, stream);
+    if (e != cudaSuccess) return e;
+  }
+  RotParams<N, K, D> p;
   p.in = in;
   p.out = out;
   p.R = R;
   const long long g = (R + kRCThreads - 1) / kRCThreads;
   if (g > 0x7fffffffLL) return cudaErrorInvalidValue;
   const size_t smem = sizeof(double) * kRCThreads * K;
-  ensure_smem_attr(reinterpret_cast<const void*>(rotate_const<N, K>), 200 * 1024);
-  rotate_const<N, K><<<static_cast<unsigned>(g), kRCThreads, smem, stream>>>(p);
+  ensure_smem_attr(reinterpret_cast<const void*>(rotate_const<N, K, D>), 200 * 1024);
+  rotate_const<N, K, D><<<static_cast<unsigned>(g), kRCThreads, smem, stream>>>(p);
   count_launch();
   return cudaGetLastError();
+}
+
+template <int N, int K>
+cudaError_t launch_rotate_const(int d, const double* E, bool uploaded, const double* in, double* out, long long R,
+                                cudaStream_t stream) {
+  switch (d) {
+#define CB_RO(v) case v: return launch_rotate_const_at<N, K, v>(E, uploaded, in, out, R, stream);
+    CB_RO(0) CB_RO(1) CB_RO(2) CB_RO(3) CB_RO(4) CB_RO(5) CB_RO(6) CB_RO(7)
+#undef CB_RO
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 unsigned grid_for(long long total, int threads) {
@@ -477,6 +536,27 @@ cudaError_t basis_matrix(long long k, const double* x, int size, double* out, St
                          cudaStream_t stream) {
   if (k <= 0) return cudaSuccess;
   basis_matrix_kernel<<<grid_for(k, 128), 128, 0, stream>>>(k, x, size, out, st, clamp);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t basis_matrices(int J, const long long* k, const double* const* x, const long long* size, double* out,
+                           Status* st, cudaStream_t stream) {
+  if (J < 1 || J > kMaxDims) return cudaErrorInvalidValue;
+  BasisBatch p{};
+  p.J = J;
+  p.st = st;
+  p.kcum[0] = 0;
+  long long off = 0;
+  for (int d = 0; d < J; ++d) {
+    p.x[d] = x[d];
+    p.out[d] = out + off;
+    p.size[d] = static_cast<int>(size[d]);
+    p.kcum[d + 1] = p.kcum[d] + k[d];
+    off += k[d] * size[d];
+  }
+  if (p.kcum[J] <= 0) return cudaSuccess;
+  basis_batch_kernel<<<grid_for(p.kcum[J], 128), 128, 0, stream>>>(p);
   count_launch();
   return cudaGetLastError();
 }
@@ -606,6 +686,19 @@ cudaError_t eval_grid(const EvalLayout& L, const double* coef, const long long* 
   auto const_ok = [&](int d) { return L.n[d] == 13 && k[d] == 25; };
   ConstSlotGuard guard(stream);
   if (guard.err != cudaSuccess) return guard.err;
+  // uniform 13 -> 25 grid: every matrix into its constant offset up front (one copy when the J
+  // matrices are contiguous, as cb_eval_grid_targets lays them out)
+  bool uniform = J * 13 * 25 <= kCETotal;
+  for (int j = 0; j < J; ++j) uniform = uniform && const_ok(j);
+  if (uniform) {
+    bool contiguous = true;
+    for (int j = 1; j < J; ++j) contiguous = contiguous && E[j] == E[0] + j * 13 * 25;
+    cudaError_t err = contiguous ? cudaMemcpyToSymbolAsync(cGridE, E[0], sizeof(double) * J * 13 * 25, 0,
+                                                           cudaMemcpyDeviceToDevice, stream)
+                                 : cudaSuccess;
+    for (int j = 0; !contiguous && j < J && err == cudaSuccess; ++j) err = upload_const<13, 25>(j, E[j], stream);
+    if (err != cudaSuccess) return err;
+  }
   int d = 0;
   while (d < J) {
     const bool pair = pairable(d);
@@ -615,12 +708,12 @@ cudaError_t eval_grid(const EvalLayout& L, const double* coef, const long long* 
     if (pair) {
       const long long n = L.n[d], kk = k[d];
       const long long R = total / ((last == J - 1 && L.q == 2) ? L.Kp : n * n);
-      if (n == 13 && kk == 25) err = launch_fused2<13, 25>(E[d], E[d + 1], cur, dst, R, stream);
-      else err = launch_fused2<5, 4>(E[d], E[d + 1], cur, dst, R, stream);
+      if (n == 13 && kk == 25) err = launch_fused2<13, 25>(d, E[d], E[d + 1], uniform, cur, dst, R, stream);
+      else err = launch_fused2<5, 4>(d, E[d], E[d + 1], false, cur, dst, R, stream);
       total = R * kk * kk;
     } else {
       const long long R = total / L.n[d];
-      err = const_ok(d) ? launch_rotate_const<13, 25>(E[d], cur, dst, R, stream)
+      err = const_ok(d) ? launch_rotate_const<13, 25>(d, E[d], uniform, cur, dst, R, stream)
                         : contract_axis(1, static_cast<int>(L.n[d]), R, 1, static_cast<int>(k[d]), E[d], cur, dst, 0, 1,
                                         k[d], stream);
       total = R * k[d];

@@ -546,6 +546,30 @@ int cb_eval_grid(int J, const int64_t* n, const double* d_coef, const int64_t* k
   return CB_OK;
 }
 
+int cb_eval_grid_targets(int J, const int64_t* n, const double* d_coef, const int64_t* k,
+                         const double* const* d_targets, double* d_E_ws, void* d_status, double* d_out,
+                         double* d_work, int64_t work_elems, void* stream) {
+  int rc = check_dims(J, n, "cb_eval_grid_targets");
+  if (rc) return rc;
+  long long kk[kMaxDims], nn[kMaxDims];
+  const double* E[kMaxDims];
+  long long off = 0;
+  for (int d = 0; d < J; ++d) {
+    if (k[d] < 1) return fail(CB_EINVAL, "cb_eval_grid_targets: empty target axis");
+    if (!d_targets || !d_targets[d]) return fail(CB_EINVAL, "cb_eval_grid_targets: null target vector");
+    kk[d] = k[d];
+    nn[d] = n[d];
+    E[d] = d_E_ws + off;
+    off += k[d] * n[d];
+  }
+  EvalLayout L = layout_of(J, n);
+  if (work_elems < eval_grid_work_elems(L, kk)) return fail(CB_EINVAL, "cb_eval_grid_targets: workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CB_CUDA(basis_matrices(J, kk, d_targets, nn, d_E_ws, static_cast<Status*>(d_status), s), "cb_eval_grid_targets");
+  CB_CUDA(eval_grid(L, d_coef, kk, E, d_out, d_work, work_elems, s), "cb_eval_grid_targets");
+  return CB_OK;
+}
+
 }  // extern "C"
 
 // ---------------------------------------------------------------------------------------------

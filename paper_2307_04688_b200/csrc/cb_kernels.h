@@ -57,6 +57,10 @@ cudaError_t contract_diagonal(long long Mcount, int n, long long R, const double
                               const double* in, long long sM, long long sL, long long sR, double* out, long long oM,
                               long long oR, Status* st, cudaStream_t stream);
 cudaError_t derivative(long long rows, int L, const double* in, double* out, cudaStream_t stream);
+// all J evaluation matrices of a structured evaluation in one launch: matrix d (k[d] x size[d])
+// at out + sum_{j<d} k[j]*size[j]; points clamped (clamp_reference) into st
+cudaError_t basis_matrices(int J, const long long* k, const double* const* x, const long long* size, double* out,
+                           Status* st, cudaStream_t stream);
 cudaError_t basis_matrix(long long k, const double* x, int size, double* out, Status* st, int clamp,
                          cudaStream_t stream);
 cudaError_t gather_index(long long rest, long long count, long long* flat, cudaStream_t stream);
