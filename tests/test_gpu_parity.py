@@ -301,6 +301,48 @@ def test_eval_grid(cuda, shape, k):
     close(cn.eval_grid(t, targets), orc.eval_grid(coef, targets))
 
 
+@pytest.mark.parametrize("shape,k", [((13, 13, 13, 13), (25, 25, 25, 25)), ((13, 13, 5, 5), (25, 25, 4, 4)),
+                                     ((5, 4, 3, 6), (2, 3, 4, 5)), ((13,) * 6, (3, 2, 25, 25, 2, 3))])
+def test_eval_grid_targets_vs_explicit_matrices(cuda, shape, k):
+    """cb_eval_grid_targets (all evaluation matrices in one launch, one constant-bank upload for
+    uniform 13 -> 25 grids) == cb_eval_grid on separately formed matrices (per-mode uploads),
+    bitwise, and == the oracle."""
+    import ctypes
+
+    from paper_2307_04688_b200 import _lib
+    from paper_2307_04688_b200.chebnd import _basis_device
+
+    rng = np.random.default_rng(77 + len(shape))
+    coef = rng.standard_normal(shape)
+    t = cn.CoefTensor([cn.make_basis(d - 1, -1.0, 1.0) for d in shape], coef)
+    targets = [np.linspace(-1, 1, kk) for kk in k]
+    J = len(shape)
+    lib = _lib.load()
+    tdev = [_lib.to_device(x) for x in targets]
+    Es = [_basis_device(tv, n, True) for tv, n in zip(tdev, shape)]  # separate allocations
+    work_elems = int(lib.cb_eval_grid_workspace(J, _lib.i64_array(shape), _lib.i64_array(k)))
+    work = _lib.empty((max(1, work_elems),))
+    out_e = _lib.empty(tuple(k))
+    eptrs = (ctypes.c_void_p * J)(*[_lib.ptr(e) for e in Es])
+    _lib.check(lib.cb_eval_grid(J, _lib.i64_array(shape), _lib.ptr(t.device_coefficients), _lib.i64_array(k), eptrs,
+                                _lib.ptr(out_e), _lib.ptr(work), work_elems, _lib.stream_handle()), "eval_grid")
+    got_e = _lib.to_host(out_e)
+    got = cn.eval_grid(t, targets)
+    assert np.array_equal(got, got_e)
+    close(got, orc.eval_grid(coef, targets))
+
+
+def test_eval_grid_target_errors(cuda):
+    t = cn.CoefTensor([cn.make_basis(4, -1.0, 1.0)] * 3, np.ones((5, 5, 5)))
+    ok = np.linspace(-1, 1, 4)
+    with pytest.raises(ValueError, match="outside"):
+        cn.eval_grid(t, [ok, ok, np.array([0.0, 1.5])])
+    with pytest.raises(ValueError, match="finite"):
+        cn.eval_grid(t, [np.array([np.nan]), ok, ok])
+    # within the clamp tolerance: clipped, no error
+    close(cn.eval_grid(t, [ok, ok, np.array([1.0 + 5e-13])]), cn.eval_grid(t, [ok, ok, np.array([1.0])]))
+
+
 @pytest.mark.parametrize("J,n,steps", [(2, 9, 7), (4, 5, 4), (6, 3, 3), (3, 17, 5), (4, 17, 2)])
 def test_advect_loop(cuda, J, n, steps):
     rng = np.random.default_rng(1000 + J * n)
