@@ -166,6 +166,43 @@ def barrier(world):
 # CPU baseline (oracle port of the reference algorithm) — the one place bench.py runs oracle/
 # ------------------------------------------------------------------------------------------------
 
+def _single_thread_mode(orc, C, pts, cores: int, budget_s: float):
+    """SURVEY.md §8d CPU mode (i), the reference as shipped: one Python thread evaluating point
+    blocks (S/solver.py with workers=1), OpenBLAS with all its threads (threadpoolctl lifts this
+    process's OPENBLAS_NUM_THREADS=1 for the duration).  Returns seconds per point."""
+    from threadpoolctl import threadpool_limits
+
+    with threadpool_limits(limits=cores, user_api="blas"):
+        n = 256
+        t0 = time.perf_counter()
+        orc.eval_points(C, pts[:n])
+        per_pt = (time.perf_counter() - t0) / n
+        n = int(min(pts.shape[0], max(256, budget_s / max(per_pt, 1e-9))))
+        t0 = time.perf_counter()
+        orc.eval_points(C, pts[:n])
+        return (time.perf_counter() - t0) / n, n
+
+
+def _with_modes(res: dict, full_units: float, tb: float, per_pt_single: float, n_single: int, cores: int,
+                pool_per_unit: float) -> dict:
+    """Attach both CPU modes; `value` is the better one (labelled in best_mode)."""
+    single_step = tb + per_pt_single * full_units
+    pool_step = res["step_seconds"]
+    res["modes"] = {
+        "pool": {"step_seconds": pool_step, "threads": cores,
+                 "what": f"ThreadPoolExecutor({cores}) over point blocks, OPENBLAS_NUM_THREADS=1 (S/solver.py:423-437)"},
+        "single": {"step_seconds": single_step, "blas_threads": cores, "points_timed": n_single,
+                   "what": "one Python thread (workers=1, as shipped), OpenBLAS default threads"},
+    }
+    if single_step < pool_step:
+        res["best_mode"] = "single"
+        res["step_seconds"] = single_step
+        res["value"] = res["value"] * pool_step / single_step
+    else:
+        res["best_mode"] = "pool"
+    return res
+
+
 def cpu_baseline(cfg: str, budget_s: float = 12.0):
     from oracle import cheb_oracle as orc
     from paper_2307_04688_b200 import workloads
@@ -195,15 +232,18 @@ def cpu_baseline(cfg: str, budget_s: float = 12.0):
         te = time.perf_counter() - t0
         # full step = one build + full_M evals, extrapolated linearly from the sample
         step_s = tb + te * (full_M / sample)
-        return {
+        res = {
             "value": full_M / step_s,
             "unit": "evals/s",
             "cores": cores,
             "kind": "port",
             "sample": f"oracle tensor_coeffs + eval of {sample} seeded points on {cores} threads "
-                      f"(ThreadPool, OPENBLAS_NUM_THREADS=1), extrapolated to M={full_M}",
+                      f"(ThreadPool, OPENBLAS_NUM_THREADS=1), extrapolated to M={full_M}; mode (i) "
+                      f"(one Python thread, multi-threaded BLAS) timed beside it, the better one is value",
             "step_seconds": step_s,
         }
+        per_single, n_single = _single_thread_mode(orc, C, pts, cores, budget_s / 3)
+        return _with_modes(res, full_M, tb, per_single, n_single, cores, te / sample)
     if cfg in ("3", "5b"):
         w = workloads.make(cfg)
         T, S = orc.advect_points(w.values.shape, w.A, w.dt)
@@ -220,14 +260,17 @@ def cpu_baseline(cfg: str, budget_s: float = 12.0):
         orc.eval_points_parallel(C, T[:sample], workers=cores, block=max(32, sample // (4 * cores)))
         te = time.perf_counter() - t0
         step_s = tb + te * (N / sample)
-        return {
+        res = {
             "value": 1.0 / step_s,
             "unit": "steps/s",
             "cores": cores,
             "kind": "port",
-            "sample": f"oracle build + {sample} of {N} advected nodes on {cores} threads, extrapolated to one step",
+            "sample": f"oracle build + {sample} of {N} advected nodes on {cores} threads, extrapolated to one step; "
+                      f"mode (i) (one Python thread, multi-threaded BLAS) timed beside it, the better one is value",
             "step_seconds": step_s,
         }
+        per_single, n_single = _single_thread_mode(orc, C, T, cores, budget_s / 3)
+        return _with_modes(res, N, tb, per_single, n_single, cores, te / sample)
     if cfg == "solve":
         from oracle import solver_oracle as so
 
