@@ -365,6 +365,41 @@ def tensor_coeffs_device(samples_dev, shape, out=None, status=None):
     return out
 
 
+class BuildEvalGraph:
+    """tensor_coeffs + eval_points for fixed shapes and fixed device buffers, captured once as a
+    CUDA graph and replayed: the per-sweep refit + evaluate of the solver (S/solver.py:441-449,
+    388-397) as ONE submission, for loops whose steps are too small to amortise per-call host work
+    (config 1: 65,536 points of a 17 x 17 interpolant).  `samples_dev` (n_1..n_J) and `points_dev`
+    (M, J) are read at every replay (update them in place), `out` (M,) is written; no host
+    synchronisation and no status checks (validate inputs before, as tensor_coeffs does)."""
+
+    def __init__(self, shape, samples_dev, points_dev, out=None):
+        t = _lib.require_cuda()
+        self.shape = tuple(int(s) for s in shape)
+        self.samples, self.points = samples_dev, points_dev
+        self.coef = _lib.empty((_lib.eval_layout(self.shape)["elems"],))
+        self.out = out if out is not None else _lib.empty((int(points_dev.shape[0]),))
+        side = t.cuda.Stream()
+        side.wait_stream(t.cuda.current_stream())
+        with t.cuda.stream(side):
+            self._enqueue()  # warm-up outside the capture: smem attributes, tensor-map encoder
+        t.cuda.current_stream().wait_stream(side)
+        t.cuda.synchronize()
+        self.graph = t.cuda.CUDAGraph()
+        n0 = int(_lib.load().cb_kernel_launches())
+        with t.cuda.graph(self.graph, capture_error_mode="thread_local"):
+            self._enqueue()
+        self.kernels_per_replay = int(_lib.load().cb_kernel_launches()) - n0  # own kernels in the graph
+
+    def _enqueue(self):
+        tensor_coeffs_device(self.samples, self.shape, out=self.coef)
+        _eval_points_device(self.shape, self.coef, self.points, check=False, out=self.out)
+
+    def replay(self):
+        self.graph.replay()
+        return self.out
+
+
 def stack_coeffs(samples, bases) -> TensorStack:
     """tensor_coeffs for (n_1..n_J, N_P) stacked samples (S/chebnd.py:193-206)."""
     bases = tuple(bases)

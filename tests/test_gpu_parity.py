@@ -396,3 +396,25 @@ def test_config4_full_batch_subset(cuda):
     idx = np.sort(np.random.default_rng(44).choice(w.points.shape[0], 1 << 14, replace=False))
     ref = orc.eval_points_parallel(orc.tensor_coeffs(w.values), w.points[idx])
     close(got[idx], ref)
+
+
+@pytest.mark.parametrize("cfg,M,n", [("1", 65_536, None), ("2", 4096, 9), ("4", 2048, 5)])
+def test_build_eval_graph(cuda, cfg, M, n):
+    """BuildEvalGraph (build + evaluate captured once, replayed) == the eager calls, bitwise, and
+    follows in-place updates of its input buffers."""
+    from paper_2307_04688_b200 import _lib
+    from paper_2307_04688_b200.chebnd import _eval_points_device, tensor_coeffs_device
+
+    w = workloads.make(cfg, M=M, n=n)
+    shape = (w.n,) * w.J
+    vals = _lib.to_device(w.values).clone()
+    pts = _lib.to_device(w.points).clone()
+    g = cn.BuildEvalGraph(shape, vals, pts)
+    assert g.kernels_per_replay >= 2
+    eager = _eval_points_device(shape, tensor_coeffs_device(vals, shape), pts, check=False)
+    assert np.array_equal(_lib.to_host(g.replay()), _lib.to_host(eager))
+    close(_lib.to_host(g.out), orc.eval_points(orc.tensor_coeffs(w.values), w.points))
+    vals.mul_(2.0)
+    pts.mul_(0.5)
+    got = _lib.to_host(g.replay())
+    close(got, orc.eval_points(orc.tensor_coeffs(2.0 * w.values), 0.5 * w.points))
