@@ -246,30 +246,41 @@ int cb_eval_points_host(int J, const int64_t* n, const double* d_coef, int64_t M
   std::lock_guard<std::mutex> lock(g_pipe_mutex);
   Pipe* p = nullptr;
   CB_CUDA(pipe_for_device(&p), "cb_eval_points_host");
-  // chunk plan: ramp up 2^15, 2^16, 2^17 and down 2^17, 2^16 (the first upload and the last
+  // chunk plan: ramp up ~2^15, 2^16, 2^17 and down ~2^17, 2^16 (the first upload and the last
   // download are the only exposed transfers), equal middle chunks of about 2^18 points (several
-  // evaluator waves each); at most 16 chunks
+  // evaluator waves each); at most 16 chunks.  Every chunk but the last is a whole number of
+  // evaluator waves (64-point tiles x SMs), so no chunk ends in a partly idle wave.
   long long bounds[kPipeMaxChunks + 1];
   int nch = 0;
   {
+    const long long W = 64LL * num_sms();
+    auto waves = [&](long long v) { return (v + W - 1) / W * W; };
     long long sizes[kPipeMaxChunks];
     long long rem = M;
     int nh = 0, nt = 0;
     long long head[3], tail[2];
     for (long long s0 : {1LL << 15, 1LL << 16, 1LL << 17}) {
       if (rem <= 0) break;
-      head[nh] = rem < s0 ? rem : s0;
+      head[nh] = rem < waves(s0) ? rem : waves(s0);
       rem -= head[nh++];
     }
     for (long long s0 : {1LL << 16, 1LL << 17}) {
       if (rem <= (1LL << 18)) break;
-      tail[nt++] = s0;
-      rem -= s0;
+      tail[nt++] = waves(s0);
+      rem -= waves(s0);
     }
     long long nmid = rem > 0 ? (rem + (1LL << 18) - 1) >> 18 : 0;
     if (nmid > kPipeMaxChunks - nh - nt) nmid = kPipeMaxChunks - nh - nt;
     for (int i = 0; i < nh; ++i) sizes[nch++] = head[i];
-    for (long long i = 0; i < nmid; ++i) sizes[nch++] = rem / nmid + (i < rem % nmid ? 1 : 0);
+    {
+      const long long each = nmid > 0 ? waves((rem + nmid - 1) / nmid) : 0;
+      long long left = rem;
+      for (long long i = 0; i < nmid && left > 0; ++i) {
+        const long long sz = (i + 1 == nmid || left < each) ? left : each;
+        sizes[nch++] = sz;
+        left -= sz;
+      }
+    }
     for (int i = nt - 1; i >= 0; --i) sizes[nch++] = tail[i];
     bounds[0] = 0;
     for (int c = 0; c < nch; ++c) bounds[c + 1] = bounds[c] + sizes[c];
