@@ -182,7 +182,11 @@ __device__ __forceinline__ void consumer_sync_n(int nthreads) {
 
 // Row-contraction evaluator shape: 16 consumer warps + producer + builder + finisher, stages of
 // kRcRows coefficient rows.
-constexpr int kRcConsumers = 16;
+#ifndef CB_RC_NT
+#define CB_RC_NT 4
+#endif
+constexpr int kRcNT = CB_RC_NT;                       // n-tiles (8 points) per consumer warp
+constexpr int kRcConsumers = 4 * (8 / kRcNT);         // 4 row groups x (64 / (8 NT)) point groups
 constexpr int kRcThreads = (kRcConsumers + 3) * 32;
 #ifndef CB_RC_ROWS
 #define CB_RC_ROWS 128

@@ -22,7 +22,8 @@ template <int NL, int MTK, int KT>
 __global__ void __launch_bounds__(kRcThreads, 1)
     eval_rc_kernel(const __grid_constant__ EvalParams p, const __grid_constant__ DmmaSmem sm,
                    const __grid_constant__ CUtensorMap amap) {
-  constexpr int NCW = kRcConsumers, NT = 2, kRows = kRcRows, KS = kRows / 16;  // KS k-steps per warp per stage
+  constexpr int NCW = kRcConsumers, NT = kRcNT, kRows = kRcRows, KS = kRows / 16;  // KS k-steps per warp per stage
+  constexpr int NGR = 8 / NT;   // point groups (8*NT points each) per row group
   constexpr int J = NL + 1;
   constexpr int KTMAX = (KT < 0) ? 3 : KT;        // DFMA tail columns (compile-time when KT >= 0)
   const int ktail = (KT < 0) ? p.ktail : KT;
@@ -131,9 +132,9 @@ __global__ void __launch_bounds__(kRcThreads, 1)
   }
 
   // consumers: warp = (row group rg: kRows/4 rows of each stage) x (point group ng: 16 points)
-  const int rg = warp >> 2, ng = warp & 3;
+  const int rg = warp / NGR, ng = warp % NGR;
   const int gq = lane >> 2, tq = lane & 3;
-  const int pcol = ng * 16 + gq;  // B-fragment column (point) of this lane (+ nt*8)
+  const int pcol = ng * 8 * NT + gq;  // B-fragment column (point) of this lane (+ nt*8)
   const int R = static_cast<int>(p.R);
   int slot = 0, it = 0;
   unsigned phase = 0;
@@ -237,13 +238,13 @@ __global__ void __launch_bounds__(kRcThreads, 1)
         phase ^= 1;
       }
     }
-    // tile end: contract k with T_k(x_{J-1}):  lane holds U'[k = m*8 + gq][p = ng*16 + nt*8 + 2tq + i]
+    // tile end: contract k with T_k(x_{J-1}):  lane holds U'[k = m*8 + gq][p = ng*8*NT + nt*8 + 2tq + i]
     double vp[NT][2];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const int pp = ng * 16 + nt * 8 + 2 * tq + i;
+        const int pp = ng * 8 * NT + nt * 8 + 2 * tq + i;
         double v = 0.0;
 #pragma unroll
         for (int m = 0; m < MTK; ++m) v = fma(acc[m][nt][i], Tsb[p.toff[J - 1] + (m * 8 + gq) * kTP + pp], v);
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(kRcThreads, 1)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int i = 0; i < 2; ++i) Rb[rg * kP + ng * 16 + nt * 8 + 2 * tq + i] = vp[nt][i];
+        for (int i = 0; i < 2; ++i) Rb[rg * kP + ng * 8 * NT + nt * 8 + 2 * tq + i] = vp[nt][i];
     }
     if (tq == 0) {
 #pragma unroll
