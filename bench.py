@@ -2,18 +2,23 @@
 """Benchmark of the fp64 tensor-Chebyshev hot path (BASELINE.json metric: Chebyshev evals/s and
 game time-steps/s, fp64, 1/2/4/8 B200 vs CPU).
 
-Default workload = BASELINE configs[1] ("config 2"): J=3, n=33 (35,937 coefficients), node values
-exp(-sum b_j (x_j - c_j)^2), M = 2^20 scattered points per GPU.  One step = build the coefficient
-tensor from the node values (K1) + evaluate it at the M points (K2).  `value` = evals/s of the
-whole job (weak scaling: every rank evaluates its own 2^20 points), measured with CUDA events
+Default workload = the largest single-GPU BASELINE configuration, configs[3] ("config 4"): J=5,
+n=17 (1,419,857 coefficients, 11.4 MB), node values exp(sum sin(pi a_j x_j)), ONE batch of
+M = 2^24 scattered points, sharded across the N GPUs (strong scaling, as BASELINE.json's config
+says).  One step = build the coefficient tensor from the node values (K1) + evaluate it at the
+rank's share of the M points (K2).  `value` = evals/s of the whole job, measured with CUDA events
 per step, max over ranks.  `e2e` = the same through the public API with host (pinned) inputs and
 outputs, H2D / D2H inside the timed region.  --config selects the other BASELINE configs
-(3 / 5b report steps/s of the time loop; 5a reports structured evals/s).
+(2 = J=3 n=33 M=2^20, 1 = J=2 n=17; 3 / 5b report steps/s of the time loop; 5a reports
+structured evals/s; solve = the collocation solver).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
 
-Under torchrun (N > 1) each rank drives one GPU; the loop configs shard nodes and all-gather
-node values over NCCL once per step.
+--gpus N > 1 without a torchrun environment re-launches itself under torch.distributed.run with N
+ranks on 127.0.0.1 (or exits non-zero when fewer than N GPUs are visible); under torchrun each rank
+drives one GPU.  The scattered configs shard points (coefficients built replicated on every rank
+from the same node values: no data-path collective); the loop configs shard node slabs and fuse
+the per-step exchange into the evaluator's NVLink peer stores.
 """
 
 from __future__ import annotations
@@ -203,7 +208,40 @@ def _with_modes(res: dict, full_units: float, tb: float, per_pt_single: float, n
     return res
 
 
+def host_info() -> dict:
+    """CPU provenance for the baseline: model, core counts, numpy / BLAS versions."""
+    info = {"cpu_model": None, "nproc": os.cpu_count(), "affinity_cores": None, "numpy": np.__version__,
+            "blas": None}
+    try:
+        info["affinity_cores"] = len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        pass
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    info["cpu_model"] = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        from threadpoolctl import threadpool_info
+
+        blas = [f"{d.get('internal_api')} {d.get('version')} ({d.get('threading_layer')}, "
+                f"{d.get('architecture')})" for d in threadpool_info() if d.get("user_api") == "blas"]
+        info["blas"] = "; ".join(blas) or None
+    except Exception:  # noqa: BLE001 - provenance only
+        pass
+    return info
+
+
 def cpu_baseline(cfg: str, budget_s: float = 12.0):
+    res = _cpu_baseline(cfg, budget_s)
+    res["host"] = host_info()
+    return res
+
+
+def _cpu_baseline(cfg: str, budget_s: float):
     from oracle import cheb_oracle as orc
     from paper_2307_04688_b200 import workloads
 
@@ -232,14 +270,17 @@ def cpu_baseline(cfg: str, budget_s: float = 12.0):
         te = time.perf_counter() - t0
         # full step = one build + full_M evals, extrapolated linearly from the sample
         step_s = tb + te * (full_M / sample)
+        extrap = sample < full_M
         res = {
             "value": full_M / step_s,
             "unit": "evals/s",
             "cores": cores,
             "kind": "port",
             "sample": f"oracle tensor_coeffs + eval of {sample} seeded points on {cores} threads "
-                      f"(ThreadPool, OPENBLAS_NUM_THREADS=1), extrapolated to M={full_M}; mode (i) "
-                      f"(one Python thread, multi-threaded BLAS) timed beside it, the better one is value",
+                      f"(ThreadPool, OPENBLAS_NUM_THREADS=1)"
+                      + (f", EXTRAPOLATED linearly to M={full_M}" if extrap else f" (full M={full_M})")
+                      + "; mode (i) (one Python thread, multi-threaded BLAS) timed beside it, the better one is value",
+            "extrapolated": extrap,
             "step_seconds": step_s,
         }
         per_single, n_single = _single_thread_mode(orc, C, pts, cores, budget_s / 3)
@@ -260,18 +301,23 @@ def cpu_baseline(cfg: str, budget_s: float = 12.0):
         orc.eval_points_parallel(C, T[:sample], workers=cores, block=max(32, sample // (4 * cores)))
         te = time.perf_counter() - t0
         step_s = tb + te * (N / sample)
+        extrap = sample < N
         res = {
             "value": 1.0 / step_s,
             "unit": "steps/s",
             "cores": cores,
             "kind": "port",
-            "sample": f"oracle build + {sample} of {N} advected nodes on {cores} threads, extrapolated to one step; "
-                      f"mode (i) (one Python thread, multi-threaded BLAS) timed beside it, the better one is value",
+            "sample": f"oracle build + {sample} of {N} advected nodes on {cores} threads"
+                      + (", EXTRAPOLATED linearly to one step" if extrap else " (one full step)")
+                      + "; mode (i) (one Python thread, multi-threaded BLAS) timed beside it, the better one is value",
+            "extrapolated": extrap,
             "step_seconds": step_s,
         }
         per_single, n_single = _single_thread_mode(orc, C, T, cores, budget_s / 3)
         return _with_modes(res, N, tb, per_single, n_single, cores, te / sample)
     if cfg == "solve":
+        from threadpoolctl import threadpool_limits
+
         from oracle import solver_oracle as so
 
         spec = solve_spec()
@@ -279,38 +325,78 @@ def cpu_baseline(cfg: str, budget_s: float = 12.0):
                     rho=spec.rho, h=spec.h, P_max=spec.P_max, U_max=spec.U_max, Np=spec.Np, Nu=spec.Nu,
                     tol=spec.tol, max_iters=spec.max_iters)
         S = so.Solver(g)
-        t0 = time.perf_counter()
-        S.solve(max_iters=20)
-        per = (time.perf_counter() - t0) / 20
-        n_s = int(max(20, min(5000, budget_s / max(per, 1e-9))))
-        t0 = time.perf_counter()
-        S.solve(max_iters=n_s)
-        per = (time.perf_counter() - t0) / n_s
+
+        def per_sweep(**kw):
+            t0 = time.perf_counter()
+            S.solve(max_iters=20, **kw)
+            per = (time.perf_counter() - t0) / 20
+            n_s = int(max(20, min(5000, budget_s / 2 / max(per, 1e-9))))
+            t0 = time.perf_counter()
+            S.solve(max_iters=n_s, **kw)
+            return (time.perf_counter() - t0) / n_s, n_s
+
+        # mode (ii): the reference's block-parallel sweep (workers = cores, one node block per
+        # worker per player, S/solver.py:412-438), one BLAS thread each
+        per_pool, n_pool = per_sweep(workers=cores, blocks=cores)
+        # mode (i): workers=1 (the reference default), BLAS with all cores
+        with threadpool_limits(limits=cores, user_api="blas"):
+            per_single, n_single = per_sweep()
+        best = "single" if per_single <= per_pool else "pool"
+        per = min(per_single, per_pool)
         return {
             "value": 1.0 / per,
             "unit": "sweeps/s",
-            "cores": 1,
+            "cores": cores,
             "kind": "port",
-            "sample": f"oracle solver (numpy restatement of S/solver.py, one thread as the reference's "
-                      f"workers=1 default): first {n_s} sweeps of the same solve",
+            "sample": f"oracle solver (numpy restatement of S/solver.py): first {n_single} / {n_pool} sweeps of the "
+                      f"same solve in mode (i) workers=1 + {cores}-thread BLAS and mode (ii) ThreadPool({cores}) over "
+                      f"(player, node block) tasks, 1 BLAS thread; value = the better mode",
+            "best_mode": best,
+            "modes": {"single": {"step_seconds": per_single * SOLVE_SWEEPS, "sweeps_timed": n_single},
+                      "pool": {"step_seconds": per_pool * SOLVE_SWEEPS, "sweeps_timed": n_pool,
+                               "threads": cores}},
             "step_seconds": per * SOLVE_SWEEPS,
         }
-    # 5a structured
+    # 5a structured: build + the full 25^6 grid, both modes, nothing extrapolated
+    from concurrent.futures import ThreadPoolExecutor
+
+    from threadpoolctl import threadpool_limits
+
     w = workloads.make("5a")
+    k = w.params["k"]
     t0 = time.perf_counter()
     C = orc.tensor_coeffs(w.values)
-    k = 25
-    # sample: grid restricted to the first 5 targets of the first axis (1/5 of the work), x5
-    targets = [w.targets[0][:5]] + list(w.targets[1:])
-    orc.eval_grid(C, targets)
-    el = time.perf_counter() - t0
-    step_s = el * (k / 5)
+    tb = time.perf_counter() - t0
+    # mode (ii): ThreadPool(cores) over single first-axis targets, one BLAS thread each
+    out = np.empty((k,) * 6)
+
+    def slab(i):
+        out[i] = orc.eval_grid(C, [w.targets[0][i:i + 1]] + list(w.targets[1:]))[0]
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=cores) as ex:
+        list(ex.map(slab, range(k)))
+    t_pool = tb + time.perf_counter() - t0
+    del out
+    # mode (i): one Python thread, BLAS on all cores
+    with threadpool_limits(limits=cores, user_api="blas"):
+        t0 = time.perf_counter()
+        r = orc.eval_grid(C, w.targets)
+        t_single = tb + time.perf_counter() - t0
+    del r
+    best = "single" if t_single <= t_pool else "pool"
+    step_s = min(t_single, t_pool)
     return {
         "value": k ** 6 / step_s,
         "unit": "evals/s",
-        "cores": 1,
+        "cores": cores,
         "kind": "port",
-        "sample": "oracle build + eval_grid on a 5x25^5 slice of the 25^6 grid (numpy matmul, 1 BLAS thread), x5",
+        "sample": f"oracle build + eval_grid of the full {k}^6 grid (not extrapolated) in mode (i) one Python thread + "
+                  f"{cores}-thread BLAS and mode (ii) ThreadPool({cores}) over first-axis targets, 1 BLAS thread; "
+                  f"value = the better mode",
+        "best_mode": best,
+        "modes": {"single": {"step_seconds": t_single}, "pool": {"step_seconds": t_pool, "threads": cores}},
+        "extrapolated": False,
         "step_seconds": step_s,
     }
 
@@ -330,10 +416,13 @@ def run_reference(args):
         return
     cfg = args.config
     steps = []
+    # each step is a bounded sample of the workload, sized so the whole --steps/--warmup run ends
+    # within a few minutes (extrapolation flagged in cpu_baseline.sample)
+    per_step = min(args.cpu_budget, max(2.0, 150.0 / max(1, args.steps)))
     for _ in range(args.warmup):
-        cpu_baseline(cfg, budget_s=2.0)
+        cpu_baseline(cfg, budget_s=1.0)
     for _ in range(args.steps):
-        steps.append(cpu_baseline(cfg, budget_s=args.cpu_budget))
+        steps.append(cpu_baseline(cfg, budget_s=per_step))
     vals = [s["value"] for s in steps]
     v = statistics.median(vals)
     base = steps[0]
@@ -347,28 +436,34 @@ def run_reference(args):
         "warmup": args.warmup,
         "ms_per_step": 1000.0 * statistics.median(s["step_seconds"] for s in steps),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": scaling_of(cfg, args.scaling),
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (seeded, BASELINE.json shapes)",
-        "config": workload_config(cfg, 1),
+        "config": workload_config(cfg, 1, args.scaling),
         "cpu_baseline": {"value": v, "unit": base["unit"], "cores": base["cores"], "kind": base["kind"],
-                         "sample": base["sample"]},
+                         "sample": base["sample"], "best_mode": base.get("best_mode"),
+                         "extrapolated": base.get("extrapolated"), "host": base["host"]},
         "e2e": {"value": v, "unit": base["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def workload_config(cfg: str, world: int):
-    from paper_2307_04688_b200 import workloads  # noqa: F401
+def scaling_of(cfg: str, scaling: str) -> str:
+    if cfg in ("1", "2", "4"):
+        return scaling
+    return "weak" if cfg == "solve" else "strong"
 
+
+def workload_config(cfg: str, world: int, scaling: str = "strong"):
+    per = "per GPU" if scaling == "weak" else "total, sharded across the GPUs"
     desc = {
-        "1": {"workload": "config1: J=2 n=17 build + eval at M=65,536 points/GPU (step = one CUDA-graph replay of "
-                           "the build + evaluation, BuildEvalGraph)", "J": 2, "n": 17, "M": 65_536},
-        "2": {"workload": "config2: J=3 n=33 build + eval at M=2^20 points/GPU", "J": 3, "n": 33, "M": 1 << 20},
+        "1": {"workload": f"config1: J=2 n=17 build + eval at M=65,536 points {per} (step = one CUDA-graph "
+                           "replay of the build + evaluation, BuildEvalGraph)", "J": 2, "n": 17, "M": 65_536},
+        "2": {"workload": f"config2: J=3 n=33 build + eval at M=2^20 points {per}", "J": 3, "n": 33, "M": 1 << 20},
         "3": {"workload": "config3: J=4 n=17 advected-node time step (build + eval of 83,521 nodes)", "J": 4,
               "n": 17, "M": 17 ** 4},
-        "4": {"workload": "config4: J=5 n=17 build + eval at M=2^24 points/GPU", "J": 5, "n": 17, "M": 1 << 24},
+        "4": {"workload": f"config4: J=5 n=17 build + eval at M=2^24 points {per}", "J": 5, "n": 17, "M": 1 << 24},
         "5a": {"workload": "config5a: J=6 n=13 build + structured eval on a 25^6 grid", "J": 6, "n": 13,
                "M": 25 ** 6},
         "5b": {"workload": "config5b: J=6 n=13 advected-node time step (4,826,809 nodes)", "J": 6, "n": 13,
@@ -378,9 +473,16 @@ def workload_config(cfg: str, world: int):
                   "J": 2, "n": 9, "M": 81},
     }[cfg]
     d = dict(desc)
-    d["parallelism"] = (f"dp{world}" if cfg in ("1", "2", "4", "5a") else
-                        "replicas" if cfg == "solve" else
-                        f"node-shard{world}+peer-store" if world > 1 else "node-shard1")
+    if cfg in ("1", "2", "4"):
+        d["parallelism"] = (f"dp{world}: contiguous point shards ({'one M batch split' if scaling == 'strong' else 'M per rank'}); "
+                            "coefficient tensor built replicated on every rank from the same node values "
+                            "(a 0.03-0.15 ms build, cheaper than an all-gather), no data-path collective")
+    elif cfg == "5a":
+        d["parallelism"] = f"dp{world}: first target axis sharded, outputs stay sharded, build replicated"
+    elif cfg == "solve":
+        d["parallelism"] = "replicas"
+    else:
+        d["parallelism"] = f"node-shard{world}+peer-store" if world > 1 else "node-shard1"
     d["l2_flush"] = "256 MiB write between timed steps"
     return d
 
@@ -414,10 +516,20 @@ def run_ours(args):
         w = workloads.make(cfg)
         J, n = w.J, w.n
         shape = (n,) * J
-        M = w.M
-        # every rank evaluates its own block of M points (weak scaling); rank r uses a shifted
-        # copy of the seeded points so ranks do distinct work
-        pts_host = np.ascontiguousarray(np.roll(w.points, rank * 977, axis=0))
+        if args.scaling == "strong":
+            # ONE batch of M points split into contiguous shards (BASELINE config 4: "points
+            # sharded across 1/2/4/8 GPUs"); the job's units are the M points
+            from paper_2307_04688_b200.dist import shard_range
+
+            pa, pb, _ = shard_range(w.M, rank, world)
+            pts_host = np.ascontiguousarray(w.points[pa:pb])
+            job_units = w.M
+        else:
+            # every rank evaluates its own block of M points; rank r uses a shifted copy of the
+            # seeded points so ranks do distinct work
+            pts_host = np.ascontiguousarray(np.roll(w.points, rank * 977, axis=0))
+            job_units = world * w.M
+        M = pts_host.shape[0]
         vals_dev = _lib.to_device(w.values)
         pts_dev = _lib.to_device(pts_host)
         L = _lib.eval_layout(shape)
@@ -499,7 +611,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         clk = clocks.stop()
         t_total = max_over_ranks(sum(step_ms) / 1000.0, world, torch)
-        value = world * M * args.steps / t_total
+        value = job_units * args.steps / t_total
         # parity spot-check of this run's output (rank 0, small subset, oracle as checker)
         flops_pt = algorithmic_eval_flops(J, n)
         eval_s = statistics.mean(eval_ms) / 1000.0
@@ -548,7 +660,7 @@ def run_ours(args):
             res = cn.eval_points(cn.tensor_coeffs(vals_pin, bases), pts_pin)  # returns pinned host tensor
         torch.cuda.synchronize()
         e2e_s = max_over_ranks(time.perf_counter() - t0, world, torch)
-        e2e = {"value": world * M * args.steps / e2e_s, "unit": "evals/s",
+        e2e = {"value": job_units * args.steps / e2e_s, "unit": "evals/s",
                "h2d_bytes_per_step": int(vals_pin.numel() * 8 + pts_pin.numel() * 8),
                "d2h_bytes_per_step": int(res.numel() * 8 + 16)}
         # parity of the e2e result against the device-timed output and the oracle on a subset
@@ -814,11 +926,11 @@ def run_ours(args):
             "warmup": args.warmup,
             "ms_per_step": ms_per_step,
             "higher_is_better": True,
-            "scaling": "weak" if cfg in ("1", "2", "4", "solve") else "strong",
+            "scaling": scaling_of(cfg, args.scaling),
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (seeded numpy, BASELINE.json shapes; no dataset)",
-            "config": workload_config(cfg, world),
+            "config": workload_config(cfg, world, args.scaling),
             "e2e": e2e,
             "gpu_launches": launches,
             "roofline": roofline,
@@ -850,16 +962,48 @@ def ncu_traffic(kernel: str, cfg: str):
         return None
 
 
+def relaunch_under_torchrun(args) -> int:
+    """--gpus N > 1 outside torchrun: re-run this script as N ranks (one per GPU) under
+    torch.distributed.run on 127.0.0.1; fails loudly when fewer than N GPUs are visible."""
+    import socket
+    import subprocess
+
+    if args.impl == "ours":
+        import torch
+
+        have = torch.cuda.device_count() if torch.cuda.is_available() else 0
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible CUDA devices, found {have}",
+                  file=sys.stderr, flush=True)
+            return 2
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="2", choices=["1", "2", "3", "4", "5a", "5b", "solve"])
+    ap.add_argument("--config", default="4", choices=["1", "2", "3", "4", "5a", "5b", "solve"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="scattered configs: split one M batch across the GPUs (strong) or M per GPU (weak)")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU work per baseline sample")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    world = int(os.environ.get("WORLD_SIZE", "0") or 0)
+    if world == 0 and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(args))
+    if world and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr, flush=True)
+        sys.exit(2)
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":

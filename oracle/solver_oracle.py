@@ -250,40 +250,49 @@ class Solver:
         """Per-player coefficient tensors of the node values (order-F reshape, S/solver.py:441-449)."""
         return [tensor_coeffs(values[i].reshape(self.shape, order="F")) for i in range(self.game.J)]
 
-    def best_response(self, i: int, coefs: list[np.ndarray], policy: np.ndarray):
-        """All nodes of player i (S/solver.py:359-409); returns (u, v, clamped count)."""
+    def best_response(self, i: int, coefs: list[np.ndarray], policy: np.ndarray, sl: slice = slice(None)):
+        """Player i on the node block `sl` (_best_response_block, S/solver.py:359-409); returns
+        (u, v, clamped count) for the block."""
         g = self.game
         pw = self.players[i]
-        n = self.nodes.shape[0]
-        cur = pw.coeffs
+        nodes = self.nodes[sl]
+        n = nodes.shape[0]
+        cur = pw.coeffs[sl]
         for j, size in zip(pw.others, pw.other_sizes):
-            Bj = row_basis(policy[j] * (2.0 / g.U_max) - 1.0, size)            # (n, size)
+            Bj = row_basis(policy[j, sl] * (2.0 / g.U_max) - 1.0, size)         # (n, size)
             cur = np.einsum("pl,plr->pr", Bj, cur.reshape(n, size, -1))
         dr = np.einsum("kl,plc->pkc", pw.B0, cur.reshape(n, pw.K, g.J))     # drift at own nodes
-        succ = self.nodes[:, None, :] + g.h * dr
+        succ = nodes[:, None, :] + g.h * dr
         clipped = np.clip(succ, 0.0, g.P_max)
         clamped = int(np.count_nonzero(clipped != succ))
         pts = clipped.reshape(-1, g.J) * (2.0 / g.P_max) - 1.0
         v_next = eval_points(coefs[i], pts).reshape(n, pw.K)
-        obj = g.delta * (pw.stage + v_next)
+        obj = g.delta * (pw.stage[sl] + v_next)
         if not np.isfinite(obj).all():
             raise FloatingPointError("non-finite objective sample in sweep")
         fit = obj @ pw.M0.T
-        x, f = maximise_rows(fit, policy[i] * (2.0 / g.U_max) - 1.0)
+        x, f = maximise_rows(fit, policy[i, sl] * (2.0 / g.U_max) - 1.0)
         return (x + 1.0) * (0.5 * g.U_max), f, clamped
 
-    def sweep(self, coefs, policy):
+    def sweep(self, coefs, policy, executor=None, blocks: int = 1):
+        """One sweep over (player, node block) tasks (_run_sweep, S/solver.py:412-438): serial, or
+        on a ThreadPoolExecutor with disjoint writes when `executor` is given."""
         J = self.game.J
         n = self.nodes.shape[0]
         u = np.empty((J, n))
         v = np.empty((J, n))
-        clamped = 0
-        for i in range(J):
-            u[i], v[i], c = self.best_response(i, coefs, policy)
-            clamped += c
-        return u, v, clamped
+        size = -(-n // max(1, blocks))
+        tasks = [(i, slice(a, min(n, a + size))) for i in range(J) for a in range(0, n, size)]
 
-    def solve(self, values=None, policy=None, max_iters: int | None = None):
+        def run(t):
+            i, sl = t
+            u[i, sl], v[i, sl], c = self.best_response(i, coefs, policy, sl)
+            return c
+
+        counts = list(executor.map(run, tasks)) if executor is not None else [run(t) for t in tasks]
+        return u, v, int(sum(counts))
+
+    def solve(self, values=None, policy=None, max_iters: int | None = None, workers: int = 1, blocks: int = 1):
         """Fixed-point driver (S/solver.py:495-570): returns dict of the EquilibriumResult fields."""
         g = self.game
         n = self.nodes.shape[0]
@@ -292,8 +301,13 @@ class Solver:
         coefs = self.refit(v)
         targets = n * sum(p.K for p in self.players) * g.J
         hist, clamp_frac, converged, it = [], 0.0, False, 0
+        ex = None
+        if workers > 1:
+            from concurrent.futures import ThreadPoolExecutor
+
+            ex = ThreadPoolExecutor(max_workers=workers)
         for it in range(1, (max_iters or g.max_iters) + 1):
-            u_new, v_new, cl = self.sweep(coefs, u)
+            u_new, v_new, cl = self.sweep(coefs, u, ex, blocks)
             clamp_frac = max(clamp_frac, cl / targets)
             d = np.max(np.abs(v_new - v), axis=1)
             hist.append(d)
@@ -302,6 +316,8 @@ class Solver:
             if float(d.max()) < g.tol:
                 converged = True
                 break
+        if ex is not None:
+            ex.shutdown()
         return dict(converged=converged, iterations=it, values=v, policy=u, coefs=coefs,
                     history=np.array(hist).reshape(-1, g.J), clamp_fraction=clamp_frac)
 

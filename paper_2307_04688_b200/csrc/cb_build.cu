@@ -613,6 +613,9 @@ __global__ void zero_pad_kernel(double* out, long long R, long long R8, long lon
 // written in the eval layout described by evl.
 cudaError_t transform_axes(int ndim, const long long* shape, int a0, int a1, const double* in, double* out,
                            Status* st, int check_finite, const EvalLayout* evl, cudaStream_t stream) {
+  // the status block is optional (header): without one there is nowhere to report a non-finite
+  // sample, so the kernels must not touch it
+  if (st == nullptr) check_finite = 0;
   if (a0 >= a1) {
     // nothing to transform: plain copy
     long long total = 1;

@@ -322,6 +322,14 @@ static int fill_advect(int J, const double* A, double dt, const double* lo, cons
   return CB_OK;
 }
 
+static int check_node_range(int J, const int64_t* n, int64_t node_begin, int64_t count, const char* who) {
+  long long N = 1;
+  for (int d = 0; d < J; ++d) N *= n[d];
+  if (node_begin < 0 || count < 0 || node_begin > N || count > N - node_begin)
+    return fail(CB_EINVAL, std::string(who) + ": node range [node_begin, node_begin + count) outside the grid");
+  return CB_OK;
+}
+
 int cb_eval_advected(int J, const int64_t* n, const double* d_coef, int64_t node_begin, int64_t count,
                      const double* A, double dt, const double* lo, const double* hi, int source, double* d_out,
                      void* stream) {
@@ -329,6 +337,8 @@ int cb_eval_advected(int J, const int64_t* n, const double* d_coef, int64_t node
   if (rc) return rc;
   for (int d = 0; d < J; ++d)
     if (n[d] > 64) return fail(CB_EINVAL, "cb_eval_advected: mode size above 64 not supported");
+  rc = check_node_range(J, n, node_begin, count, "cb_eval_advected");
+  if (rc) return rc;
   EvalLayout L = layout_of(J, n);
   AdvectSpec adv;
   rc = fill_advect(J, A, dt, lo, hi, source, adv);
@@ -349,6 +359,8 @@ int cb_eval_advected_peers(int J, const int64_t* n, const double* d_coef, int64_
   if (G < 1 || G > 8 || !d_full) return fail(CB_EINVAL, "cb_eval_advected_peers: need 1..8 destination buffers");
   for (int r = 0; r < G; ++r)
     if (!d_full[r]) return fail(CB_EINVAL, "cb_eval_advected_peers: null destination buffer");
+  rc = check_node_range(J, n, node_begin, count, "cb_eval_advected_peers");
+  if (rc) return rc;
   EvalLayout L = layout_of(J, n);
   AdvectSpec adv;
   rc = fill_advect(J, A, dt, lo, hi, source, adv);
@@ -418,6 +430,95 @@ static cudaError_t loop_step(const EvalLayout& L, const long long* shape, const 
   return eval_points(L, coef, N, nullptr, &adv, vout, nullptr, 0, s);
 }
 
+// Instantiated step-pair graphs of cb_advect_loop, cached per (device, shape, buffers, drift):
+// the graph bakes in its buffer pointers and the advection parameters, so a repeated call with the
+// same arguments replays the executable graph instead of re-capturing it.  Each entry owns the
+// private capture/replay stream (the caller's stream may be the legacy default stream, which
+// cannot be captured) and the event ordering it after / before the caller's stream.  Guarded by
+// g_loop_mutex (the one per-device context cache the header allows).
+struct LoopGraphKey {
+  int device, J;
+  long long shape[kMaxDims];
+  const void* ptrs[4];
+  AdvectSpec adv;
+  bool operator==(const LoopGraphKey& o) const { return std::memcmp(this, &o, sizeof(*this)) == 0; }
+};
+struct LoopGraph {
+  LoopGraphKey key;
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  unsigned long long last_use = 0;
+};
+constexpr int kLoopGraphCache = 8;
+std::mutex g_loop_mutex;
+LoopGraph g_loop_graphs[kLoopGraphCache];
+unsigned long long g_loop_clock = 0;
+
+static void loop_graph_release(LoopGraph& g) {
+  if (g.cs) cudaStreamSynchronize(g.cs);  // an in-flight replay finishes before its exec goes
+  if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (g.ev) cudaEventDestroy(g.ev);
+  if (g.cs) cudaStreamDestroy(g.cs);
+  g = LoopGraph{};
+}
+
+static cudaError_t loop_graph_build(LoopGraph& g, const EvalLayout& L, const long long* shape, const AdvectSpec& adv,
+                                    double* v, double* tmp, double* coef, Status* st, long long N) {
+  cudaError_t e = cudaStreamCreateWithFlags(&g.cs, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g.ev, cudaEventDisableTiming);
+  cudaGraph_t graph = nullptr;
+  if (e == cudaSuccess) e = cudaStreamBeginCapture(g.cs, cudaStreamCaptureModeThreadLocal);
+  if (e == cudaSuccess) {
+    cudaError_t e1 = loop_step(L, shape, adv, v, tmp, coef, st, N, g.cs);
+    cudaError_t e2 = e1 == cudaSuccess ? loop_step(L, shape, adv, tmp, v, coef, st, N, g.cs) : e1;
+    cudaError_t e3 = cudaStreamEndCapture(g.cs, &graph);
+    e = e1 != cudaSuccess ? e1 : e2 != cudaSuccess ? e2 : e3;
+  }
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&g.exec, graph, 0);
+  if (graph) cudaGraphDestroy(graph);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    loop_graph_release(g);
+  }
+  return e;
+}
+
+static cudaError_t loop_graph_run(const EvalLayout& L, const long long* shape, const AdvectSpec& adv, double* v,
+                                  double* tmp, double* coef, Status* st, long long N, int pairs, cudaStream_t user) {
+  LoopGraphKey key;
+  std::memset(&key, 0, sizeof(key));
+  cudaError_t e = cudaGetDevice(&key.device);
+  if (e != cudaSuccess) return e;
+  key.J = L.J;
+  for (int d = 0; d < L.J; ++d) key.shape[d] = shape[d];
+  key.ptrs[0] = v;
+  key.ptrs[1] = tmp;
+  key.ptrs[2] = coef;
+  key.ptrs[3] = st;
+  key.adv = adv;
+  std::lock_guard<std::mutex> lock(g_loop_mutex);
+  LoopGraph* g = nullptr;
+  for (auto& c : g_loop_graphs)
+    if (c.exec && c.key == key) g = &c;
+  if (!g) {
+    g = &g_loop_graphs[0];
+    for (auto& c : g_loop_graphs)
+      if (!c.exec || c.last_use < g->last_use) g = &c;
+    if (g->exec) loop_graph_release(*g);
+    g->key = key;
+    e = loop_graph_build(*g, L, shape, adv, v, tmp, coef, st, N);
+    if (e != cudaSuccess) return e;
+  }
+  g->last_use = ++g_loop_clock;
+  e = cudaEventRecord(g->ev, user);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(g->cs, g->ev, 0);
+  for (int s = 0; s < pairs && e == cudaSuccess; ++s) e = cudaGraphLaunch(g->exec, g->cs);
+  if (e == cudaSuccess) e = cudaEventRecord(g->ev, g->cs);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(user, g->ev, 0);
+  return e;
+}
+
 int cb_advect_loop(int J, const int64_t* n, double* d_values, double* d_tmp, double* d_coef, int steps,
                    const double* A, double dt, const double* lo, const double* hi, void* d_status, int use_graph,
                    void* stream) {
@@ -447,31 +548,7 @@ int cb_advect_loop(int J, const int64_t* n, double* d_values, double* d_tmp, dou
       CB_CUDA(loop_step(L, shape, adv, d_tmp, d_values, d_coef, st, N, user), "cb_advect_loop");
     }
   } else {
-    // Capture one step pair on a private stream (the caller's stream may be the legacy default
-    // stream, which cannot be captured), then replay it; ordered after / before `user` by events.
-    cudaStream_t cs;
-    CB_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "cb_advect_loop: stream");
-    cudaEvent_t ev;
-    CB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cb_advect_loop: event");
-    CB_CUDA(cudaEventRecord(ev, user), "cb_advect_loop: record");
-    CB_CUDA(cudaStreamWaitEvent(cs, ev, 0), "cb_advect_loop: wait");
-    cudaGraph_t graph;
-    cudaGraphExec_t exec;
-    CB_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal), "cb_advect_loop: capture");
-    cudaError_t e1 = loop_step(L, shape, adv, d_values, d_tmp, d_coef, st, N, cs);
-    cudaError_t e2 = loop_step(L, shape, adv, d_tmp, d_values, d_coef, st, N, cs);
-    cudaError_t e3 = cudaStreamEndCapture(cs, &graph);
-    if (e1 != cudaSuccess) return cuda_fail(e1, "cb_advect_loop: capture step");
-    if (e2 != cudaSuccess) return cuda_fail(e2, "cb_advect_loop: capture step");
-    if (e3 != cudaSuccess) return cuda_fail(e3, "cb_advect_loop: end capture");
-    CB_CUDA(cudaGraphInstantiate(&exec, graph, 0), "cb_advect_loop: instantiate");
-    for (int s = 0; s < pairs; ++s) CB_CUDA(cudaGraphLaunch(exec, cs), "cb_advect_loop: launch");
-    CB_CUDA(cudaEventRecord(ev, cs), "cb_advect_loop: record");
-    CB_CUDA(cudaStreamWaitEvent(user, ev, 0), "cb_advect_loop: wait");
-    cudaGraphExecDestroy(exec);
-    cudaGraphDestroy(graph);
-    cudaEventDestroy(ev);
-    cudaStreamDestroy(cs);  // destruction is deferred until the stream's work completes
+    CB_CUDA(loop_graph_run(L, shape, adv, d_values, d_tmp, d_coef, st, N, pairs, user), "cb_advect_loop");
   }
   if (steps & 1) {
     CB_CUDA(loop_step(L, shape, adv, d_values, d_tmp, d_coef, st, N, user), "cb_advect_loop");

@@ -185,3 +185,32 @@ def test_peer_loop_matches_single(shape, world):
     for r in range(world):
         assert np.array_equal(res[r][0], ref1), (r, np.abs(res[r][0] - ref1).max())
         assert np.array_equal(res[r][1], ref2), (r, np.abs(res[r][1] - ref2).max())
+
+
+def test_cuda_backend_barrier_takes_nccl_branch(monkeypatch):
+    """CudaStepBackend.barrier under an nccl group (world > 1) is the stream-ordered 1-element NCCL
+    all-reduce on the compute stream (no host synchronize, no host barrier); under gloo it is the
+    device synchronize + host barrier.  Host logic only: torch.distributed is stubbed."""
+    from paper_2307_04688_b200 import _lib
+    from paper_2307_04688_b200.loop import CudaStepBackend
+
+    calls = []
+    monkeypatch.setattr(_lib, "require_cuda", lambda: torch)
+    be = object.__new__(CudaStepBackend)  # no device buffers needed for the branch logic
+    be._flag = object()
+    monkeypatch.setattr(dist, "is_initialized", lambda: True)
+    monkeypatch.setattr(dist, "get_world_size", lambda group=None: 2)
+    monkeypatch.setattr(dist, "all_reduce", lambda t, group=None: calls.append(("all_reduce", t)))
+    monkeypatch.setattr(dist, "barrier", lambda group=None: calls.append(("barrier", None)))
+    monkeypatch.setattr(torch.cuda, "synchronize", lambda *a, **k: calls.append(("synchronize", None)))
+    monkeypatch.setattr(dist, "get_backend", lambda group=None: "nccl")
+    be.barrier()
+    assert calls == [("all_reduce", be._flag)]
+    calls.clear()
+    monkeypatch.setattr(dist, "get_backend", lambda group=None: "gloo")
+    be.barrier()
+    assert [c[0] for c in calls] == ["synchronize", "barrier"]
+    calls.clear()
+    monkeypatch.setattr(dist, "get_world_size", lambda group=None: 1)
+    be.barrier()
+    assert calls == []
