@@ -3,19 +3,22 @@
 // Reference: tensor_coeffs S/chebnd.py:162-190 applies the 1-D DCT-I (cheb_transform,
 // S/cheb1d.py:138-170, an rfft of the even extension) along every mode, rotating the axes
 // in between.  Mathematically that is J mode-n products with the n x n matrix
-// M0 = diag(s) B^T diag(w) of S/solver.py:162-171.  Here the mode products are applied to
-// shared-memory tiles that span a GROUP of consecutive modes, so a tensor is read from and
-// written to global memory once per group (1 pass for tensors up to ~12k elements, 2 passes for
-// the J=5/J=6 BASELINE shapes, with the intermediate resident in the 126 MB L2) rather than once
-// per mode.  Each fiber product uses the even/odd fold M0[l, N-k] = (-1)^l M0[l, k], which halves
-// the flops (n/2 FMA per element per mode).
-//
-// Two pass flavours:
-//   contiguous : the group ends with the last tensor mode; a tile is one contiguous block of
-//                prod(n_group) values.  Output may be written in the pitched "eval layout"
-//                (rows of K values padded to Kp) consumed by the K2 evaluator.
-//   strided    : a group of leading/middle modes; a tile is prod(n_group) rows x ct contiguous
-//                inner columns.  Runs in place after the first pass.
+// M0 = diag(s) B^T diag(w) of S/solver.py:162-171.  Every path below applies those products with
+// the even/odd fold M0[l, N-k] = (-1)^l M0[l, k] (n/2 FMA per element per mode) and the same
+// per-fiber FMA order, so all paths give bitwise-identical coefficients.  Paths, by shape:
+//   * <= 6,144 entries, every mode n <= 34: ONE single-CTA launch (small_build_kernel) — the
+//     whole tensor in shared memory (config 1, the solver's fields, most test shapes);
+//   * full builds with every mode the same n in {5, 9, 13, 17, 33} (the BASELINE tensors 33^3,
+//     17^4, 17^5, 13^6): mode-GROUP passes (group_pass_kernel), 2 launches — the trailing <= 3
+//     modes on contiguous slabs read once from the dense samples and written to the eval layout,
+//     then the leading modes in place on column tiles; the tensor crosses the L2 <-> SM boundary
+//     twice instead of J times;
+//   * any other shape with modes n <= 34: one fiber pass per mode (fiber_pass_kernel /
+//     fiber_inner_kernel, thread per fiber, L2-resident between passes), in place on the output;
+//   * modes n > 34: smem group passes with runtime sizes (build_pass_kernel).
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include "cb_common.cuh"
 #include "cb_kernels.h"
 
@@ -611,6 +614,358 @@ __global__ void zero_pad_kernel(double* out, long long R, long long R8, long lon
 // Transform the consecutive axes [a0, a1) of a dense C-order array `shape` (ndim dims).
 // When `evl` is non-null the call is a full tensor build (a0 = 0, a1 = ndim) and the output is
 // written in the eval layout described by evl.
+// ------------------------------------------------------------------------------------------
+// Mode-group passes for full builds of equal-size modes (every BASELINE tensor above the
+// single-CTA size): the J mode products are applied in 2 launches instead of J, each CTA holding
+// one tile that spans a GROUP of up to 3 modes in shared memory, so the tensor crosses the
+// L2 <-> SM boundary twice instead of J times (the intermediate stays in the 126 MB L2).
+//   pass 1 (contiguous): the trailing group — a tile is S whole slabs of N^G contiguous samples,
+//                        read once from the dense input (non-finite check), written to the eval
+//                        layout with its pad columns (and, by block 0, the pad rows);
+//   pass 2+ (strided)  : a group of leading modes in place on the eval layout — a tile is N^G rows
+//                        x CW contiguous inner columns (32-128 B row segments).
+// Per fiber the arithmetic is exactly the fiber passes' (same folded constant-bank matrix, same
+// FMA order), so the result is bitwise identical to the per-mode path.
+// ------------------------------------------------------------------------------------------
+constexpr int kGroupMaxTile = 9216;        // doubles of one tile (72 KB: 2-3 CTAs per SM)
+constexpr int kGroupMaxSlab = 6144;        // contiguous flavour: N^G per slab
+constexpr int kGroupMaxG = 3;
+// fibers per thread per mode: 2 measured faster for n = 13 (13^6: 51 -> 43 us), 1 for 17 and 33
+template <int TN>
+constexpr int group_fpt() { return TN == 13 ? 2 : 1; }
+
+// One thread per fiber per mode (nf = E / N threads): straight-line code like the fiber passes
+// (a loop over fibers lets the compiler hoist the ~N^2/2 matrix constants into registers and
+// spill).  Each mode of the group reads its own copy of the folded matrix so the constants are
+// not shared (and kept live) across the modes either.  Group size G and tile width CW are
+// template parameters, so every fiber stride is a compile-time constant (immediate smem offsets,
+// division by constants) — the kernel was issue-bound on index arithmetic before.
+template <int TN>
+constexpr int group_threads_max() { return TN > 24 ? 256 : 512; }
+
+constexpr int ipow(int b, int e) { return e == 0 ? 1 : b * ipow(b, e - 1); }
+
+template <int TN>
+struct GroupParams {
+  const double* in;
+  double* out;
+  Status* st;
+  int check_finite;
+  int vec;                  // 16-byte aligned rows: cp.async / stores two doubles at a time
+  // contiguous flavour (CW = 1): tile t = slabs [t*S, t*S+S) of A, written in the output layout
+  // (rows of K values at pitch Kp)
+  int S;
+  long long A;
+  int K, Kp;
+  FastDiv fd_Kp;
+  long long R, R8;          // pad rows [R, R8) zeroed by block 0 (eval layout only)
+  // strided flavour: tile t = (a, column tile), a < A, rows N^G x CW columns of inner extent Cn
+  long long Cn, ctiles;
+  double M[kGroupMaxG][TN * (TN / 2 + 1)];   // folded matrix per mode, row pitch N/2 + 1
+};
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(double* dst, const double* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <int TN, int STRIDE, bool CHECK>
+__device__ __forceinline__ void group_fiber(double* s, const double* M, bool& ok) {
+  constexpr int N = TN - 1, H = TN / 2, P = H + 1;
+  double v[TN];
+#pragma unroll
+  for (int k = 0; k < TN; ++k) v[k] = s[k * STRIDE];
+  if constexpr (CHECK) {
+#pragma unroll
+    for (int k = 0; k < TN; ++k) ok &= isfinite(v[k]);
+  }
+  double e[H > 0 ? H : 1], o[H > 0 ? H : 1];
+#pragma unroll
+  for (int k = 0; k < H; ++k) {
+    e[k] = v[k] + v[N - k];
+    o[k] = v[k] - v[N - k];
+  }
+#pragma unroll
+  for (int l = 0; l <= N; ++l) {
+    double acc = 0.0;
+    if ((l & 1) == 0) {
+#pragma unroll
+      for (int k = 0; k < H; ++k) acc = fma(M[l * P + k], e[k], acc);
+      if constexpr (TN & 1) acc = fma(M[l * P + H], v[H], acc);
+    } else {
+#pragma unroll
+      for (int k = 0; k < H; ++k) acc = fma(M[l * P + k], o[k], acc);
+    }
+    s[l * STRIDE] = acc;
+  }
+}
+
+template <int TN, int G, int CW, int g>
+__device__ __forceinline__ void group_mode(double* tile, int nf, const GroupParams<TN>& p, bool& ok) {
+  constexpr int STRIDE = ipow(TN, G - 1 - g) * CW;
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < group_fpt<TN>(); ++j) {
+    const int f = threadIdx.x + j * blockDim.x;
+    if (f < nf) {
+      const int o = f / STRIDE, i = f - (f / STRIDE) * STRIDE;
+      group_fiber<TN, STRIDE, g == G - 1 && CW == 1>(tile + o * TN * STRIDE + i, p.M[g], ok);
+    }
+  }
+  if constexpr (g > 0) group_mode<TN, G, CW, (g > 0 ? g - 1 : 0)>(tile, nf, p, ok);
+}
+
+template <int TN, int G, int CW>
+__global__ void __launch_bounds__(group_threads_max<TN>()) group_pass_kernel(const __grid_constant__ GroupParams<TN> p) {
+  constexpr int P = ipow(TN, G);
+  extern __shared__ __align__(16) double tile[];
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const long long t = blockIdx.x;
+  bool ok = true;
+  if constexpr (CW == 1) {
+    // ---------------- contiguous flavour: S whole slabs of the dense input ----------------
+    const long long a0 = t * p.S;
+    const int valid = static_cast<int>(min(static_cast<long long>(p.S), p.A - a0)) * P;
+    const double* src = p.in + a0 * P;
+    if (p.vec) {
+      const int vend = valid & ~1;   // a last tile of an odd number of odd slabs: one tail element
+      for (int e = 2 * tid; e < vend; e += 2 * nth) cp_async16(tile + e, src + e);
+      if (tid == 0 && vend < valid) cp_async8(tile + vend, src + vend);
+    } else {
+      for (int e = tid; e < valid; e += nth) cp_async8(tile + e, src + e);
+    }
+    cp_async_wait_all();
+    // innermost mode first (the per-mode passes' order: bitwise-identical results)
+    group_mode<TN, G, CW, G - 1>(tile, valid / TN, p, ok);
+    if (p.check_finite && !ok) atomicAdd(&p.st->nonfinite, 1u);   // first mode's loads checked
+    __syncthreads();
+    // rows of K values -> output rows of pitch Kp (pad columns written as zeros)
+    const int rows = valid / p.K;
+    const long long row0 = a0 * P / p.K;
+    double* dst = p.out + row0 * p.Kp;
+    const int n_out = rows * p.Kp;
+    if (p.vec) {
+      for (int z = 2 * tid; z < n_out; z += 2 * nth) {
+        uint32_t row, col;
+        p.fd_Kp.divmod(static_cast<uint32_t>(z), row, col);
+        const double* srow = tile + row * p.K;
+        double2 v;
+        v.x = (static_cast<int>(col) < p.K) ? srow[col] : 0.0;
+        v.y = (static_cast<int>(col) + 1 < p.K) ? srow[col + 1] : 0.0;
+        *reinterpret_cast<double2*>(dst + z) = v;
+      }
+    } else {
+      for (int z = tid; z < n_out; z += nth) {
+        uint32_t row, col;
+        p.fd_Kp.divmod(static_cast<uint32_t>(z), row, col);
+        dst[z] = (static_cast<int>(col) < p.K) ? tile[row * p.K + col] : 0.0;
+      }
+    }
+    if (t == 0 && p.R8 > p.R) {
+      double* pad = p.out + p.R * p.Kp;
+      const long long n = (p.R8 - p.R) * p.Kp;
+      for (long long z = tid; z < n; z += nth) pad[z] = 0.0;
+    }
+  } else {
+    // ---------------- strided flavour: N^G rows x CW columns, in place ----------------
+    constexpr int E = P * CW;
+    const long long a = t / p.ctiles;
+    const long long c0 = (t - a * p.ctiles) * CW;
+    const long long gbase = a * P * p.Cn + c0;
+    const bool full = c0 + CW <= p.Cn;
+    const double* src = p.in + gbase;
+    if (full && p.vec) {
+      for (int e = 2 * tid; e < E; e += 2 * nth) {
+        const int r = e / CW, cc = e % CW;
+        cp_async16(tile + e, src + static_cast<long long>(r) * p.Cn + cc);
+      }
+    } else {
+      for (int e = tid; e < E; e += nth) {
+        const int r = e / CW, cc = e % CW;
+        if (c0 + cc < p.Cn) cp_async8(tile + e, src + static_cast<long long>(r) * p.Cn + cc);
+        else tile[e] = 0.0;
+      }
+    }
+    cp_async_wait_all();
+    group_mode<TN, G, CW, G - 1>(tile, E / TN, p, ok);
+    __syncthreads();
+    double* dst = p.out + gbase;
+    if (full && p.vec) {
+      for (int e = 2 * tid; e < E; e += 2 * nth) {
+        const int r = e / CW, cc = e % CW;
+        *reinterpret_cast<double2*>(dst + static_cast<long long>(r) * p.Cn + cc) =
+            *reinterpret_cast<const double2*>(tile + e);
+      }
+    } else {
+      for (int e = tid; e < E; e += nth) {
+        const int r = e / CW, cc = e % CW;
+        if (c0 + cc < p.Cn) dst[static_cast<long long>(r) * p.Cn + cc] = tile[e];
+      }
+    }
+  }
+}
+
+// Host-side description of one group pass (independent of the template size).
+struct GroupPass {
+  int contiguous, G, P, E, S, K, Kp, CW, vec;
+  long long A, R, R8, Cn, tiles;
+};
+
+template <int TN>
+constexpr bool group_templated() { return TN == 5 || TN == 9 || TN == 13 || TN == 17 || TN == 33; }
+
+template <int TN, int G>
+void launch_group_g(const GroupParams<TN>& p, const GroupPass& g, int threads, int bytes, cudaStream_t stream) {
+  auto go = [&](auto kern) {
+    ensure_smem_attr(reinterpret_cast<const void*>(kern), kGroupMaxTile * 8, true);
+    kern<<<static_cast<unsigned>(g.tiles), threads, bytes, stream>>>(p);
+  };
+  switch (g.CW) {
+    case 1: go(group_pass_kernel<TN, G, 1>); break;
+    case 4: go(group_pass_kernel<TN, G, 4>); break;
+    case 8: go(group_pass_kernel<TN, G, 8>); break;
+    case 16: go(group_pass_kernel<TN, G, 16>); break;
+    default: break;   // not planned
+  }
+}
+
+template <int TN>
+void launch_group(const GroupPass& g, const double* in, double* out, Status* st, int check_finite,
+                  cudaStream_t stream) {
+  if constexpr (group_templated<TN>()) {
+    GroupParams<TN> p{};
+    p.in = in;
+    p.out = out;
+    p.st = st;
+    p.check_finite = check_finite;
+    p.vec = g.vec;
+    p.S = g.S;
+    p.A = g.A;
+    p.K = g.K;
+    p.Kp = g.Kp;
+    if (g.Kp > 0) p.fd_Kp = FastDiv(static_cast<uint32_t>(g.Kp));
+    p.R = g.R;
+    p.R8 = g.R8;
+    p.Cn = g.Cn;
+    p.ctiles = g.contiguous ? 0 : (g.Cn + g.CW - 1) / g.CW;
+    constexpr int N = TN - 1, P = TN / 2 + 1;
+    for (int l = 0; l < TN; ++l)
+      for (int c = 0; c < P; ++c) {
+        const double v = (c <= N) ? transform_entry(l, c, N) : 0.0;
+        for (int k = 0; k < kGroupMaxG; ++k) p.M[k][l * P + c] = v;
+      }
+    const int nf = g.E / TN;
+    int threads = ((nf + group_fpt<TN>() - 1) / group_fpt<TN>() + 31) & ~31;
+    if (threads < 64) threads = 64;
+    const int bytes = g.E * static_cast<int>(sizeof(double));
+    if (g.G == 1) launch_group_g<TN, 1>(p, g, threads, bytes, stream);
+    else if (g.G == 2) launch_group_g<TN, 2>(p, g, threads, bytes, stream);
+    else launch_group_g<TN, 3>(p, g, threads, bytes, stream);
+    count_launch();
+  }
+}
+
+// Full build of a tensor whose modes all have size n (2 <= n <= 34) in 2-3 mode-group passes.
+// Returns false (nothing launched) when the shape does not fit the plan.
+bool group_build(int ndim, const long long* shape, const double* in, double* out, Status* st, int check_finite,
+                 const EvalLayout* evl, cudaStream_t stream, cudaError_t* err) {
+  *err = cudaSuccess;
+  if (ndim < 2 || ndim > kMaxDims) return false;
+  const int n = static_cast<int>(shape[0]);
+  if (n != 5 && n != 9 && n != 13 && n != 17 && n != 33) return false;   // group_templated<>
+  for (int d = 1; d < ndim; ++d)
+    if (shape[d] != n) return false;
+  long long pw[kMaxDims + 1];
+  pw[0] = 1;
+  for (int d = 1; d <= ndim; ++d) pw[d] = pw[d - 1] * n;
+  const long long total = pw[ndim];
+  const int q = evl ? evl->q : 0;
+  const long long K = evl ? evl->K : 1, Kp = evl ? evl->Kp : 1;
+  const long long outsz = evl ? evl->R8 * evl->Kp : total;
+  if (outsz >= (1LL << 31) || total >= (1LL << 31)) return false;
+  const int max_threads = (n > 24 ? 256 : 512) * (n == 13 ? 2 : 1);   // fibers per tile and mode
+  const long long max_tile = std::min<long long>(kGroupMaxTile, static_cast<long long>(max_threads) * n);
+  const int sms = num_sms();
+  GroupPass plan[3];
+  int np = 0;
+  // trailing group (pass 1): the largest g (>= q, < ndim) whose slab fits, preferring >= one
+  // slab per SM
+  int gt = 0;
+  for (int g = std::min(ndim - 1, kGroupMaxG); g >= 1; --g) {
+    if (g < q || pw[g] > std::min<long long>(kGroupMaxSlab, max_tile)) continue;
+    if (gt == 0) gt = g;
+    if (pw[ndim - g] >= sms) { gt = g; break; }
+  }
+  if (gt == 0) return false;
+  {
+    GroupPass& g = plan[np++];
+    g = GroupPass{};
+    g.contiguous = 1;
+    g.CW = 1;
+    g.G = gt;
+    g.P = static_cast<int>(pw[gt]);
+    g.A = pw[ndim - gt];
+    int S = 1;
+    while (2LL * S * g.P <= max_tile && (g.A + 2 * S - 1) / (2 * S) >= 2 * sms && S * g.P / n < 256) S *= 2;
+    if ((g.P & 1) && (S & 1) && S > 1) --S;
+    g.S = S;
+    g.E = S * g.P;
+    g.K = evl ? static_cast<int>(K) : g.P;
+    g.Kp = evl ? static_cast<int>(Kp) : g.P;
+    g.R = evl ? evl->R : 0;
+    g.R8 = evl ? evl->R8 : 0;
+    g.tiles = (g.A + S - 1) / S;
+    // 16-byte vectors: every tile's slab start and every output row 16-byte aligned
+    g.vec = (reinterpret_cast<uintptr_t>(in) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0 &&
+             (static_cast<long long>(S) * g.P) % 2 == 0 && g.Kp % 2 == 0 && (g.P % 2 == 0 || S % 2 == 0))
+                ? 1 : 0;
+  }
+  // leading modes [0, ndim - gt): strided groups, innermost first, in place on the output
+  for (int hi = ndim - gt; hi > 0;) {
+    int G = 0;
+    while (G < kGroupMaxG && hi - G - 1 >= 0 && pw[G + 1] * 4 <= max_tile) ++G;
+    if (G == 0 || np == 3) return false;   // more passes than the plan is worth: per-mode path
+    GroupPass& g = plan[np++];
+    g = GroupPass{};
+    g.contiguous = 0;
+    g.G = G;
+    g.P = static_cast<int>(pw[G]);
+    long long Cn = 1;
+    if (evl) {
+      for (int d = hi; d < ndim - q; ++d) Cn *= n;
+      Cn *= Kp;
+    } else {
+      Cn = pw[ndim - hi];
+    }
+    g.A = pw[hi - G];
+    int CW = 16;
+    while (CW > 4 && (g.P * CW > max_tile || g.A * ((Cn + CW - 1) / CW) < 2 * sms)) CW >>= 1;
+    if (g.P * CW > max_tile) return false;
+    g.CW = CW;
+    g.Cn = Cn;
+    g.E = g.P * CW;
+    g.tiles = g.A * ((Cn + CW - 1) / CW);
+    g.vec = (reinterpret_cast<uintptr_t>(out) % 16 == 0 && Cn % 2 == 0) ? 1 : 0;
+    hi -= G;
+  }
+  for (int i = 0; i < np; ++i) {
+    const bool ok = dispatch_fiber(n, [&](auto tag) {
+      launch_group<decltype(tag)::value>(plan[i], i == 0 ? in : out, out, st, i == 0 ? check_finite : 0, stream);
+    });
+    if (!ok) return i > 0;
+    *err = cudaGetLastError();
+    if (*err != cudaSuccess) return true;
+  }
+  return true;
+}
+
 cudaError_t transform_axes(int ndim, const long long* shape, int a0, int a1, const double* in, double* out,
                            Status* st, int check_finite, const EvalLayout* evl, cudaStream_t stream) {
   // the status block is optional (header): without one there is nowhere to report a non-finite
@@ -634,6 +989,15 @@ cudaError_t transform_axes(int ndim, const long long* shape, int a0, int a1, con
       if (shape[d] > 34) small_modes = false;
       const long long fb = total / shape[d];
       if (min_fibers < 0 || fb < min_fibers) min_fibers = fb;
+    }
+    // CB_BUILD_PERMODE=1 (experiments only): keep the per-mode fiber passes for A/B timing
+    static const bool permode = [] {
+      const char* e = std::getenv("CB_BUILD_PERMODE");
+      return e && e[0] == '1';
+    }();
+    if (a0 == 0 && a1 == ndim && total > kSmallBuild && !permode) {
+      cudaError_t gerr = cudaSuccess;
+      if (group_build(ndim, shape, in, out, st, check_finite, evl, stream, &gerr)) return gerr;
     }
     if (small_modes && min_fibers >= kFiberMinFibers && ndim <= kMaxDims + 1) {
       // strides: input dense C-order; output dense or the eval layout (leading rows x Kp pitch)

@@ -26,7 +26,7 @@ int g_attr_n[kMaxDevices];
 int g_sms[kMaxDevices];
 }  // namespace
 
-void ensure_smem_attr(const void* func, int bytes) {
+void ensure_smem_attr(const void* func, int bytes, bool max_carveout) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= kMaxDevices) return;
@@ -34,6 +34,10 @@ void ensure_smem_attr(const void* func, int bytes) {
   for (int i = 0; i < g_attr_n[dev]; ++i)
     if (g_attr[dev][i].func == func && g_attr[dev][i].bytes >= bytes) return;
   cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  // several smem-tiled CTAs per SM: ask for the whole unified L1/smem as shared memory (the
+  // driver's default carveout left room for only 1-3 such CTAs)
+  if (max_carveout)
+    cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (g_attr_n[dev] < 64) g_attr[dev][g_attr_n[dev]++] = {func, bytes};
 }
 

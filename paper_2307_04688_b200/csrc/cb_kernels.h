@@ -23,7 +23,7 @@ struct EvalLayout {
 EvalLayout make_eval_layout(int J, const long long* n);
 
 // Per-device one-time cudaFuncSetAttribute(MaxDynamicSharedMemorySize).
-void ensure_smem_attr(const void* func, int bytes);
+void ensure_smem_attr(const void* func, int bytes, bool max_carveout = false);
 int num_sms();
 // Process-wide count of kernels launched by this library (reported as gpu_launches by bench.py).
 void count_launch();

@@ -418,3 +418,28 @@ def test_build_eval_graph(cuda, cfg, M, n):
     pts.mul_(0.5)
     got = _lib.to_host(g.replay())
     close(got, orc.eval_points(orc.tensor_coeffs(2.0 * w.values), 0.5 * w.points))
+
+
+@pytest.mark.parametrize("shape", [(33, 33, 33), (17,) * 4, (17,) * 5, (13,) * 6, (9,) * 5, (5,) * 7, (13,) * 3, (17, 17, 17)])
+def test_group_build_bitwise_equals_per_mode_passes(cuda, shape):
+    """The mode-group build (2 launches for equal modes n in {5, 9, 13, 17, 33}) applies the same
+    per-fiber folded products in the same mode order (last mode first) as the one-pass-per-mode
+    path, so the coefficients are bitwise identical; the per-mode path is reached here through
+    two partial-axis transforms (cb_transform_axes over modes [k, J) then [0, k))."""
+    from paper_2307_04688_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(len(shape) * 100 + shape[0])
+    s = rng.standard_normal(shape)
+    full = cn.tensor_coeffs(s, [cn.make_basis(d - 1, -1.0, 1.0) for d in shape]).coefficients
+    J = len(shape)
+    k = J // 2
+    dev = _lib.to_device(s)
+    mid = _lib.empty(shape)
+    out = _lib.empty(shape)
+    for (a0, a1, src, dst) in ((k, J, dev, mid), (0, k, mid, out)):
+        _lib.check(lib.cb_transform_axes(J, _lib.i64_array(shape), a0, a1, _lib.ptr(src), _lib.ptr(dst), None, 0,
+                                         _lib.stream_handle()), "transform_axes")
+    per_mode = _lib.to_host(out)
+    assert np.array_equal(full, per_mode), float(np.abs(full - per_mode).max())
+    close(full, orc.tensor_coeffs(s))
