@@ -1,6 +1,8 @@
 // Internal (C++) entry points shared between the kernel translation units and the C-ABI layer.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include "cb_common.cuh"
 #include "../../include/chebnash_b200.h"
@@ -25,6 +27,8 @@ EvalLayout make_eval_layout(int J, const long long* n);
 // Per-device one-time cudaFuncSetAttribute(MaxDynamicSharedMemorySize).
 void ensure_smem_attr(const void* func, int bytes, bool max_carveout = false);
 int num_sms();
+// cuTensorMapEncodeTiled via the runtime's driver entry point (nullptr when unavailable).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();
 // Process-wide count of kernels launched by this library (reported as gpu_launches by bench.py).
 void count_launch();
 long long launch_count();
