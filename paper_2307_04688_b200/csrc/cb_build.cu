@@ -29,7 +29,8 @@ namespace {
 constexpr int kBuildThreads = 256;
 constexpr int kMaxGroup = 4;
 constexpr int kMaxTemplN = 34;   // fiber sizes with a fully unrolled register path
-constexpr int kMaxGenericN = 128;   // degree <= 127 on the generic (non-unrolled) path
+constexpr int kMaxGenericN = 128;   // degree <= 127 on the smem group path (build_pass_kernel)
+constexpr int kMaxTransformN = 1 << 16;   // larger modes: large_fiber_kernel (per-mode passes)
 
 struct PassParams {
   const double* in;
@@ -532,6 +533,114 @@ bool launch_fiber_pass(int nd, const long long* sizes, const long long* sin, con
 }
 
 
+// ------------------------------------------------------------------------------------------
+// Large modes (n > 34, any size up to the C-ABI limit): one CTA per fiber (grid-stride), the
+// fiber's folded halves e/o staged in shared memory, each thread producing outputs l with the
+// folded matrix read k-major from a device scratch table (coalesced across l).  The entries come
+// from the same transform_entry (exact integer angle reduction) and every output sums k
+// ascending then the middle sample, like fiber_fixed/fiber_generic: the same numerics at any n.
+// ------------------------------------------------------------------------------------------
+constexpr int kLargeThreads = 256;
+
+__global__ void fold_matrix_kernel(double* Mt, int n) {
+  const int N = n - 1, H = n / 2;
+  const long long total = static_cast<long long>(H + 1) * n;
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(e / n), l = static_cast<int>(e % n);
+    Mt[e] = (k <= N) ? transform_entry(l, k, N) : 0.0;
+  }
+}
+
+struct LargeParams {
+  const double* in;
+  double* out;
+  const double* Mt;       // [H+1][n] folded matrix, k-major
+  Status* st;
+  int check_finite;
+  int n;
+  int nother;
+  int nd[kMaxDims + 1];
+  long long sin[kMaxDims + 1], sout[kMaxDims + 1];
+  long long kin, kout;
+  long long fibers;
+};
+
+__global__ void __launch_bounds__(kLargeThreads) large_fiber_kernel(const __grid_constant__ LargeParams p) {
+  extern __shared__ __align__(16) double lsm[];   // e[H+1], o[H]
+  const int n = p.n, N = n - 1, H = n / 2;
+  double* e = lsm;
+  double* o = lsm + H + 1;
+  bool ok = true;
+  for (long long f = blockIdx.x; f < p.fibers; f += gridDim.x) {
+    long long oin = 0, oout = 0, rem = f;
+    for (int i = p.nother - 1; i >= 0; --i) {
+      const long long q = rem / p.nd[i], r = rem - q * p.nd[i];
+      oin += r * p.sin[i];
+      oout += r * p.sout[i];
+      rem = q;
+    }
+    __syncthreads();   // the previous fiber's outputs are written (in place) before new loads
+    for (int k = threadIdx.x; k < H; k += blockDim.x) {
+      const double a = p.in[oin + k * p.kin], b = p.in[oin + (N - k) * p.kin];
+      ok &= isfinite(a) && isfinite(b);
+      e[k] = a + b;
+      o[k] = a - b;
+    }
+    if ((n & 1) && threadIdx.x == 0) {
+      const double m = p.in[oin + H * p.kin];
+      ok &= isfinite(m);
+      e[H] = m;
+    }
+    __syncthreads();
+    for (int l = threadIdx.x; l < n; l += blockDim.x) {
+      double acc = 0.0;
+      if ((l & 1) == 0) {
+        for (int k = 0; k < H; ++k) acc = fma(p.Mt[static_cast<long long>(k) * n + l], e[k], acc);
+        if (n & 1) acc = fma(p.Mt[static_cast<long long>(H) * n + l], e[H], acc);
+      } else {
+        for (int k = 0; k < H; ++k) acc = fma(p.Mt[static_cast<long long>(k) * n + l], o[k], acc);
+      }
+      p.out[oout + l * p.kout] = acc;
+    }
+  }
+  if (p.check_finite && !ok) atomicAdd(&p.st->nonfinite, 1u);
+}
+
+// One large-mode pass (mode d of a strided tensor, folded matrix Mt prepared for sizes[d]).
+cudaError_t launch_large_pass(int nd, const long long* sizes, const long long* sin, const long long* sout, int d,
+                              const double* in, double* out, const double* Mt, Status* st, int check_finite,
+                              cudaStream_t stream) {
+  LargeParams p{};
+  p.in = in;
+  p.out = out;
+  p.Mt = Mt;
+  p.st = st;
+  p.check_finite = check_finite;
+  p.n = static_cast<int>(sizes[d]);
+  long long fibers = 1;
+  int j = 0;
+  for (int i = 0; i < nd; ++i) {
+    if (i == d) continue;
+    p.nd[j] = static_cast<int>(sizes[i]);
+    p.sin[j] = sin[i];
+    p.sout[j] = sout[i];
+    fibers *= sizes[i];
+    ++j;
+  }
+  p.nother = j;
+  p.kin = sin[d];
+  p.kout = sout[d];
+  p.fibers = fibers;
+  if (fibers <= 0) return cudaSuccess;
+  long long grid = std::min<long long>(fibers, static_cast<long long>(num_sms()) * 8);
+  const size_t bytes = sizeof(double) * (2 * static_cast<size_t>(p.n / 2) + 1);
+  if (bytes > 48 * 1024) ensure_smem_attr(reinterpret_cast<const void*>(large_fiber_kernel), static_cast<int>(bytes));
+  large_fiber_kernel<<<static_cast<unsigned>(grid), kLargeThreads, bytes, stream>>>(p);
+  count_launch();
+  return cudaGetLastError();
+}
+
 // Small tensors (<= kSmallBuild doubles, every mode n <= 34): the whole build in ONE launch of one
 // CTA — samples staged in shared memory, every mode transformed there (last mode first, the same
 // folded-matrix arithmetic as the fiber passes, so the result is bitwise identical to the
@@ -978,8 +1087,11 @@ cudaError_t transform_axes(int ndim, const long long* shape, int a0, int a1, con
     if (in != out) return cudaMemcpyAsync(out, in, sizeof(double) * total, cudaMemcpyDeviceToDevice, stream);
     return cudaSuccess;
   }
-  for (int d = a0; d < a1; ++d)
-    if (shape[d] < 1 || shape[d] > kMaxGenericN) return cudaErrorInvalidValue;
+  bool large_modes = false;
+  for (int d = a0; d < a1; ++d) {
+    if (shape[d] < 1 || shape[d] > kMaxTransformN) return cudaErrorInvalidValue;
+    if (shape[d] > kMaxGenericN) large_modes = true;
+  }
   {
     long long total = 1;
     bool small_modes = true;
@@ -999,7 +1111,7 @@ cudaError_t transform_axes(int ndim, const long long* shape, int a0, int a1, con
       cudaError_t gerr = cudaSuccess;
       if (group_build(ndim, shape, in, out, st, check_finite, evl, stream, &gerr)) return gerr;
     }
-    if (small_modes && min_fibers >= kFiberMinFibers && ndim <= kMaxDims + 1) {
+    if ((small_modes || large_modes) && min_fibers >= kFiberMinFibers && ndim <= kMaxDims + 1) {
       // strides: input dense C-order; output dense or the eval layout (leading rows x Kp pitch)
       long long sin[kMaxDims + 1], sout[kMaxDims + 1];
       long long acc = 1;
@@ -1024,7 +1136,7 @@ cudaError_t transform_axes(int ndim, const long long* shape, int a0, int a1, con
       // small tensor, all modes: one single-CTA launch (small_build_kernel)
       long long mat = 0;
       for (int d = 0; d < ndim; ++d) mat += shape[d] * (shape[d] / 2 + 1);
-      if (a0 == 0 && a1 == ndim && total <= kSmallBuild && mat <= kSmallMat) {
+      if (small_modes && a0 == 0 && a1 == ndim && total <= kSmallBuild && mat <= kSmallMat) {
         SmallBuildParams sp{};
         sp.in = in;
         sp.out = out;
@@ -1067,18 +1179,46 @@ cudaError_t transform_axes(int ndim, const long long* shape, int a0, int a1, con
       } else {
         for (int d = 0; d < ndim; ++d) sout[d] = sin[d];
       }
+      // folded matrices of the large modes: device scratch (stream-ordered pool), one per size
+      double* mats[kMaxDims + 1] = {};
+      cudaError_t err = cudaSuccess;
+      for (int d = a0; d < a1 && err == cudaSuccess; ++d) {
+        if (shape[d] <= 34) continue;
+        for (int d2 = a0; d2 < d; ++d2)
+          if (shape[d2] == shape[d]) mats[d] = mats[d2];
+        if (mats[d]) continue;
+        const long long n = shape[d], cnt = (n / 2 + 1) * n;
+        err = cudaMallocAsync(reinterpret_cast<void**>(&mats[d]), sizeof(double) * cnt, stream);
+        if (err != cudaSuccess) {
+          mats[d] = nullptr;
+          break;
+        }
+        fold_matrix_kernel<<<static_cast<unsigned>(std::min<long long>((cnt + 255) / 256, 1024)), 256, 0, stream>>>(
+            mats[d], static_cast<int>(n));
+        count_launch();
+        err = cudaGetLastError();
+      }
       const double* cur = in;
       bool first = true;
-      for (int d = a1 - 1; d >= a0; --d) {
-        cudaError_t err = cudaSuccess;
-        if (!launch_fiber_pass(ndim, shape, first ? sin : sout, sout, d, cur, out, st, first ? check_finite : 0,
-                               stream, &err))
-          return cudaErrorInvalidValue;
-        if (err != cudaSuccess) return err;
+      for (int d = a1 - 1; d >= a0 && err == cudaSuccess; --d) {
+        if (shape[d] <= 34) {
+          if (!launch_fiber_pass(ndim, shape, first ? sin : sout, sout, d, cur, out, st, first ? check_finite : 0,
+                                 stream, &err))
+            err = cudaErrorInvalidValue;
+        } else {
+          err = launch_large_pass(ndim, shape, first ? sin : sout, sout, d, cur, out, mats[d], st,
+                                  first ? check_finite : 0, stream);
+        }
         cur = out;
         first = false;
       }
-      return cudaSuccess;
+      for (int d = a0; d < a1; ++d) {
+        if (!mats[d]) continue;
+        bool shared = false;
+        for (int d2 = d + 1; d2 < a1; ++d2) shared = shared || mats[d2] == mats[d];
+        if (!shared) cudaFreeAsync(mats[d], stream);
+      }
+      return err;
     }
   }
   long long inner = 1;

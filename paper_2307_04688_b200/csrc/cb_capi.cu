@@ -6,6 +6,8 @@
 #include <atomic>
 #include <mutex>
 #include <string>
+#include <vector>
+#include <algorithm>
 #include <cuda.h>
 #include "../../include/chebnash_b200.h"
 #include "cb_common.cuh"
@@ -83,7 +85,8 @@ static int check_dims(int J, const int64_t* n, const char* fn) {
   long long total = 1;
   for (int d = 0; d < J; ++d) {
     if (n[d] < 1) return fail(CB_EINVAL, std::string(fn) + ": mode sizes must be >= 1");
-    if (n[d] > 128) return fail(CB_EINVAL, std::string(fn) + ": mode size above 128 (degree 127) is not supported");
+    if (n[d] > kMaxModeSize)
+      return fail(CB_EINVAL, std::string(fn) + ": mode size above 4096 (degree 4095) is not supported");
     total *= n[d];
     if (total > (1LL << 31)) return fail(CB_EINVAL, std::string(fn) + ": tensor larger than 2^31 elements");
   }
@@ -186,7 +189,8 @@ int cb_transform_axes(int ndim, const int64_t* shape, int a0, int a1, const doub
     if (total > (1LL << 31)) return fail(CB_EINVAL, "cb_transform_axes: array larger than 2^31 elements");
   }
   for (int d = a0; d < a1; ++d)
-    if (shape[d] > 128) return fail(CB_EINVAL, "cb_transform_axes: axis longer than 128 (degree 127) not supported");
+    if (shape[d] > kMaxModeSize)
+      return fail(CB_EINVAL, "cb_transform_axes: axis longer than 4096 (degree 4095) not supported");
   CB_CUDA(transform_axes(ndim, shp, a0, a1, d_in, d_out, static_cast<Status*>(d_status), check_finite, nullptr,
                          static_cast<cudaStream_t>(stream)),
           "cb_transform_axes");
@@ -312,6 +316,64 @@ int cb_eval_points_host(int J, const int64_t* n, const double* d_coef, int64_t M
   return CB_OK;
 }
 
+// Device node tables for advected evaluations whose modes have more nodes than the kernel
+// parameters carry (kMaxNodeTab): make_basis nodes (S/cheb1d.py:97-103, descending, ends pinned;
+// the same host arithmetic as the parameter tables) uploaded once per (device, shape, box) and
+// cached for the life of the process (a few KB each; the graph cache and in-flight launches may
+// hold the pointer, so entries are never freed).  Created synchronously: not inside a capture.
+struct NodeTable {
+  int device, J;
+  long long n[kMaxDims];
+  double lo[kMaxDims], hi[kMaxDims];
+  double* d_tab;
+  int pitch;
+};
+std::mutex g_node_mutex;
+std::vector<NodeTable> g_node_tables;
+constexpr size_t kMaxNodeTables = 1024;
+
+static int advect_node_table(int J, const int64_t* n, AdvectSpec& adv, cudaStream_t stream, const char* who) {
+  bool big = false;
+  for (int d = 0; d < J; ++d) big = big || n[d] > 64;
+  if (!big) return CB_OK;
+  int dev = 0;
+  CB_CUDA(cudaGetDevice(&dev), who);
+  std::lock_guard<std::mutex> lock(g_node_mutex);
+  for (const NodeTable& t : g_node_tables) {
+    bool same = t.device == dev && t.J == J;
+    for (int d = 0; same && d < J; ++d) same = t.n[d] == n[d] && t.lo[d] == adv.lo[d] && t.hi[d] == adv.hi[d];
+    if (same) {
+      adv.node_tab = t.d_tab;
+      adv.node_pitch = t.pitch;
+      return CB_OK;
+    }
+  }
+  if (g_node_tables.size() >= kMaxNodeTables) return fail(CB_EINVAL, std::string(who) + ": too many distinct grids");
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CB_CUDA(cudaStreamIsCapturing(stream, &cs), who);
+  if (cs != cudaStreamCaptureStatusNone)
+    return fail(CB_EINVAL, std::string(who) + ": first evaluation of a grid with > 64 nodes per mode inside a capture");
+  NodeTable t{};
+  t.device = dev;
+  t.J = J;
+  int pitch = 0;
+  for (int d = 0; d < J; ++d) {
+    t.n[d] = n[d];
+    t.lo[d] = adv.lo[d];
+    t.hi[d] = adv.hi[d];
+    pitch = std::max(pitch, static_cast<int>(n[d]));
+  }
+  t.pitch = pitch;
+  std::vector<double> h(static_cast<size_t>(J) * pitch, 0.0);
+  for (int d = 0; d < J; ++d) make_nodes(adv.lo[d], adv.hi[d], n[d], h.data() + static_cast<size_t>(d) * pitch);
+  CB_CUDA(cudaMalloc(reinterpret_cast<void**>(&t.d_tab), sizeof(double) * h.size()), who);
+  CB_CUDA(cudaMemcpy(t.d_tab, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice), who);
+  g_node_tables.push_back(t);
+  adv.node_tab = t.d_tab;
+  adv.node_pitch = pitch;
+  return CB_OK;
+}
+
 static int fill_advect(int J, const double* A, double dt, const double* lo, const double* hi, int source,
                        AdvectSpec& adv) {
   std::memset(&adv, 0, sizeof(adv));
@@ -339,13 +401,13 @@ int cb_eval_advected(int J, const int64_t* n, const double* d_coef, int64_t node
                      void* stream) {
   int rc = check_dims(J, n, "cb_eval_advected");
   if (rc) return rc;
-  for (int d = 0; d < J; ++d)
-    if (n[d] > 64) return fail(CB_EINVAL, "cb_eval_advected: mode size above 64 not supported");
   rc = check_node_range(J, n, node_begin, count, "cb_eval_advected");
   if (rc) return rc;
   EvalLayout L = layout_of(J, n);
   AdvectSpec adv;
   rc = fill_advect(J, A, dt, lo, hi, source, adv);
+  if (rc) return rc;
+  rc = advect_node_table(J, n, adv, static_cast<cudaStream_t>(stream), "cb_eval_advected");
   if (rc) return rc;
   adv.node_begin = node_begin;
   CB_CUDA(eval_points(L, d_coef, count, nullptr, &adv, d_out, nullptr, 0, static_cast<cudaStream_t>(stream)),
@@ -358,8 +420,6 @@ int cb_eval_advected_peers(int J, const int64_t* n, const double* d_coef, int64_
                            double* const* d_full, int G, void* stream) {
   int rc = check_dims(J, n, "cb_eval_advected_peers");
   if (rc) return rc;
-  for (int d = 0; d < J; ++d)
-    if (n[d] > 64) return fail(CB_EINVAL, "cb_eval_advected_peers: mode size above 64 not supported");
   if (G < 1 || G > 8 || !d_full) return fail(CB_EINVAL, "cb_eval_advected_peers: need 1..8 destination buffers");
   for (int r = 0; r < G; ++r)
     if (!d_full[r]) return fail(CB_EINVAL, "cb_eval_advected_peers: null destination buffer");
@@ -368,6 +428,8 @@ int cb_eval_advected_peers(int J, const int64_t* n, const double* d_coef, int64_
   EvalLayout L = layout_of(J, n);
   AdvectSpec adv;
   rc = fill_advect(J, A, dt, lo, hi, source, adv);
+  if (rc) return rc;
+  rc = advect_node_table(J, n, adv, static_cast<cudaStream_t>(stream), "cb_eval_advected_peers");
   if (rc) return rc;
   adv.node_begin = node_begin;
   adv.npeers = G;
@@ -528,12 +590,12 @@ int cb_advect_loop(int J, const int64_t* n, double* d_values, double* d_tmp, dou
                    void* stream) {
   int rc = check_dims(J, n, "cb_advect_loop");
   if (rc) return rc;
-  for (int d = 0; d < J; ++d)
-    if (n[d] > 64) return fail(CB_EINVAL, "cb_advect_loop: mode size above 64 not supported");
   if (steps < 0) return fail(CB_EINVAL, "cb_advect_loop: negative step count");
   EvalLayout L = layout_of(J, n);
   AdvectSpec adv;
   rc = fill_advect(J, A, dt, lo, hi, 1, adv);
+  if (rc) return rc;
+  rc = advect_node_table(J, n, adv, static_cast<cudaStream_t>(stream), "cb_advect_loop");
   if (rc) return rc;
   adv.node_begin = 0;
   long long shape[kMaxDims];

@@ -44,6 +44,8 @@ struct EvalParams {
   double lo[kMaxDims], hi[kMaxDims];
   int source;
   double nodes[kMaxDims][kMaxNodeTab];
+  const double* node_tab;   // modes above kMaxNodeTab nodes: device table [J][node_pitch] instead
+  int node_pitch;
   // fused exchange (multi-GPU loop): results go to every rank's node-value buffer through
   // NVLink peer stores instead of `out` (peers[r] already offset to this launch's first node)
   int npeers;
@@ -123,7 +125,7 @@ __device__ __forceinline__ void point_coords(const EvalParams& p, long long g, d
       const long long qd = idx / p.n[d];
       const int kd = static_cast<int>(idx - qd * p.n[d]);
       idx = qd;
-      x[d] = p.nodes[d][kd];
+      x[d] = p.node_tab ? p.node_tab[d * p.node_pitch + kd] : p.nodes[d][kd];
     }
   }
   double s = 0.0;

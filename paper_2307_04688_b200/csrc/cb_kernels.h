@@ -1,5 +1,6 @@
 // Internal (C++) entry points shared between the kernel translation units and the C-ABI layer.
 #pragma once
+#include <cmath>
 #include <cstdint>
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -8,6 +9,22 @@
 #include "../../include/chebnash_b200.h"
 
 namespace cb {
+
+// Largest mode size the C ABI accepts (degree 4095); modes above 34 / 128 take the generic paths.
+constexpr int kMaxModeSize = 4096;
+
+// make_basis nodes on [lo, hi] (S/cheb1d.py:97-103): descending, endpoints pinned exactly.
+inline void make_nodes(double lo, double hi, long long n, double* out) {
+  const long long N = n - 1;
+  for (long long k = 0; k <= N; ++k) {
+    double v;
+    if (N == 0) v = 0.5 * (lo + hi);
+    else if (k == 0) v = hi;
+    else if (k == N) v = lo;
+    else v = 0.5 * (hi - lo) * cos(3.141592653589793 * static_cast<double>(k) / static_cast<double>(N)) + 0.5 * (lo + hi);
+    out[k] = v;
+  }
+}
 
 // Eval layout of a J-mode coefficient tensor: the trailing q modes merged into K columns
 // (padded to Kp, a multiple of 4), the leading J-q modes into R rows (padded to R8, a multiple
@@ -46,6 +63,8 @@ struct AdvectSpec {
   int source;               // subtract dt*|x|^2 of the (unclipped) node
   int npeers;               // > 0: store results into peers[r][node] (full node-value buffers) instead of out
   double* peers[8];
+  const double* node_tab;   // device node table [J][node_pitch] (required when a mode has > 64 nodes)
+  int node_pitch;
 };
 const char* last_eval_plan();  // kernel / plan chosen by the last eval_points on this thread
 cudaError_t eval_points(const EvalLayout& L, const double* coef, long long M, const double* points,

@@ -73,8 +73,10 @@ def test_invalid_arguments_map_to_valueerror():
     assert rc == 1
     with pytest.raises(ValueError):
         _lib.check(rc)
-    rc = lib.cb_eval_layout(1, _lib.i64_array([200]), out)
-    assert rc == 1 and b"128" in lib.cb_last_error()
+    rc = lib.cb_eval_layout(1, _lib.i64_array([5000]), out)
+    assert rc == 1 and b"4096" in lib.cb_last_error()
+    # degree 255 (mode size 256) is in range since the large-mode transform path
+    assert lib.cb_eval_layout(1, _lib.i64_array([256]), out) == 0
 
 
 def test_no_cpu_fallback_without_cuda():

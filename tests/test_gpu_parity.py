@@ -443,3 +443,50 @@ def test_group_build_bitwise_equals_per_mode_passes(cuda, shape):
     per_mode = _lib.to_host(out)
     assert np.array_equal(full, per_mode), float(np.abs(full - per_mode).max())
     close(full, orc.tensor_coeffs(s))
+
+
+# ------------------------------------------------------------------------------------------------
+# the reference's input range: modes above 128 (large-mode transform), advected grids above 64
+# nodes per mode (device node tables) — S/cheb1d.py:138-170 and S/chebnd.py:162-190 have no limits
+# ------------------------------------------------------------------------------------------------
+
+def test_transform_large_degrees_match_direct_sum(cuda):
+    rng = np.random.default_rng(256)
+    for N in (129, 150, 200, 255, 256, 511):
+        s = rng.standard_normal(N + 1)
+        c = cn.coeffs_from_samples(s, cn.make_basis(N, -1.0, 1.0)).coefficients
+        np.testing.assert_allclose(c, orc.direct_transform(s), atol=1e-12)
+        close(c, orc.cheb_transform(s))
+
+
+@pytest.mark.parametrize("shape", [(200,), (130, 3), (3, 257), (150, 40), (40, 150, 2), (129, 34)])
+def test_build_and_eval_large_modes(cuda, shape):
+    rng = np.random.default_rng(sum(shape))
+    s = rng.standard_normal(shape)
+    bases = [cn.make_basis(d - 1, -1.0, 1.0) for d in shape]
+    t = cn.tensor_coeffs(s, bases)
+    C = orc.tensor_coeffs(s)
+    close(t.coefficients, C)
+    pts = 2.0 * rng.random((3000, len(shape))) - 1.0
+    close(cn.eval_points(t, pts), orc.eval_points(C, pts))
+    close(cn.eval_full(t, pts[0]), orc.eval_full(C, pts[0]))
+
+
+def test_build_large_mode_rejects_nonfinite(cuda):
+    s = np.ones((300,))
+    s[17] = np.inf
+    with pytest.raises(ValueError, match="finite"):
+        cn.tensor_coeffs(s, [cn.make_basis(299, -1.0, 1.0)])
+
+
+@pytest.mark.parametrize("shape,steps", [((100,), 4), ((70, 5), 3), ((5, 66, 3), 2)])
+def test_advect_loop_above_64_nodes(cuda, shape, steps):
+    J = len(shape)
+    rng = np.random.default_rng(900 + sum(shape))
+    A = rng.uniform(-0.5, 0.5, (J, J))
+    axes = [workloads.grid_axes(n, 1)[0] for n in shape]
+    V0 = np.exp(sum(np.sin(np.pi * 1.1 * g) for g in np.meshgrid(*axes, indexing="ij")))
+    bases = [cn.make_basis(n - 1, 0.0, 1.0) for n in shape]
+    got = cn.advect_loop(V0, bases, A, 0.01, steps)
+    close(got, orc.advect_loop(V0, A, 0.01, steps))
+    assert np.array_equal(got, cn.advect_loop(V0, bases, A, 0.01, steps, use_graph=False))
