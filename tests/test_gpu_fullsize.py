@@ -127,3 +127,15 @@ def test_config5b_stepwise_t0_t9_t19(cuda):
         _report(f"config5b_step{target}->{target + 1}", V_next.ravel()[idx], ref, step=target)
         V = V_next
         t += 1
+
+
+def test_config5a_grid_nonsymmetric_targets(cuda):
+    """The J = 6 13 -> 25 plan on targets that are NOT symmetric about 0 (the unfolded kernels),
+    full 25^6 grid against the oracle."""
+    w = workloads.make("5a")
+    rng = np.random.default_rng(5150)
+    targets = [np.sort(2.0 * rng.random(25) - 1.0) for _ in range(6)]
+    t = cn.tensor_coeffs(w.values, _bases(w.J, w.n))
+    got = cn.eval_grid(t, targets)
+    ref = orc.eval_grid(orc.tensor_coeffs(w.values), targets)
+    _report("config5a_grid_25^6_nonsymmetric_targets", got, ref)
