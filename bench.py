@@ -44,7 +44,7 @@ if ROOT not in sys.path:
 
 METRIC = "Chebyshev evals/sec & game time-steps/sec (fp64) at 1/2/4/8 B200 vs CPU"
 FP64_PEAK_FILE = os.path.join(ROOT, "profiles", "fp64_peak_r01.json")
-NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+NCU_SUMMARY = os.path.join(ROOT, "profiles", "ncu_summary_r02.json")
 
 
 def algorithmic_eval_flops(J: int, n: int) -> int:
@@ -642,7 +642,7 @@ def run_ours(args):
         }
         build_bytes = 16 * n ** J
         roofline_build = {
-            "bound": "hbm", "kernel": "fiber_inner_kernel + fiber_pass_kernel (K1 mode passes)", "achieved": build_bytes / build_s / 1e9,
+            "bound": "hbm", "kernel": build_kernels(cfg), "achieved": build_bytes / build_s / 1e9,
             "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": build_bytes / build_s / 1e9 / peaks["hbm_gbs"],
             "algorithmic": f"16*n^J = {build_bytes} bytes per build", "ms": build_s * 1000.0,
         }
@@ -780,7 +780,7 @@ def run_ours(args):
             "traffic": ncu_traffic("eval_dmma_kernel", cfg),
         }
         build_bytes = 16 * N
-        extra = {"roofline_build": {"bound": "hbm", "kernel": "fiber_inner_kernel + fiber_pass_kernel (K1 mode passes)",
+        extra = {"roofline_build": {"bound": "hbm", "kernel": build_kernels(cfg),
                                     "achieved": build_bytes / build_s / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                                     "frac": build_bytes / build_s / 1e9 / peaks["hbm_gbs"], "ms": build_s * 1e3},
                  "loop_steps_per_timed_step": inner}
@@ -945,6 +945,16 @@ def run_ours(args):
         import torch.distributed as dist
 
         dist.destroy_process_group()
+
+
+def build_kernels(cfg: str) -> str:
+    """The K1 launches of this config's build (cb_build.cu plan)."""
+    return {"1": "small_build_kernel (one single-CTA launch)",
+            "2": "group_pass_kernel<33,1,1> + <33,2,4> (2 mode-group launches)",
+            "3": "group_pass_kernel<17,2,1> + <17,2,4> (2 mode-group launches)",
+            "4": "group_pass_kernel<17,3,1> + <17,2,16> (2 mode-group launches)",
+            "5a": "group_pass_kernel<13,3,1> + <13,3,4> (2 mode-group launches)",
+            "5b": "group_pass_kernel<13,3,1> + <13,3,4> (2 mode-group launches)"}.get(cfg, "K1 build")
 
 
 def ncu_traffic(kernel: str, cfg: str):
