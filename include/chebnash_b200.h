@@ -21,7 +21,16 @@
  *     (cheb1d.py:127-135, chebnd.py:179-185).  The caller zeroes it before the call.
  *   - Dense tensors are C-order (n_1, ..., n_J) fp64 (chebnd.py:33-54).  Coefficients consumed by
  *     the evaluators are in the "eval layout" described by cb_eval_layout().
- *   - Re-entrant: no global mutable state apart from per-device kernel attributes.
+ *   - Re-entrant, with two documented exceptions to "no global mutable state": mutex-guarded
+ *     per-device caches (kernel attributes, cb_advect_loop's instantiated graphs, advected-node
+ *     tables for modes above 64 nodes), and the __constant__ slot that holds cb_eval_grid's
+ *     evaluation matrices (every DFMA of the structured passes reads them as constant operands).
+ *     Eager cb_eval_grid / cb_eval_grid_targets calls on different streams and threads are
+ *     ordered through that slot by an internal event guard; a cb_eval_grid captured into a CUDA
+ *     graph bypasses the guard, so such a graph must not be replayed concurrently with another
+ *     cb_eval_grid (captured or eager) on another stream.
+ *   - Input range: 1 <= J <= 8 modes, mode sizes 1..4096 (degree <= 4095), at most 2^31
+ *     elements per tensor.
  */
 #ifndef CHEBNASH_B200_H
 #define CHEBNASH_B200_H

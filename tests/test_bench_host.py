@@ -39,7 +39,7 @@ def test_cpu_baseline_records_host_provenance():
 
 def test_cpu_baseline_solve_both_modes():
     r = _bench().cpu_baseline("solve", budget_s=0.5)
-    assert set(r["modes"]) == {"single", "pool"} and r["cores"] >= 1
+    assert set(r["modes"]) == {"single", "single_1blas", "pool"} and r["cores"] >= 1
     assert r["best_mode"] in r["modes"]
 
 
