@@ -490,3 +490,48 @@ def test_advect_loop_above_64_nodes(cuda, shape, steps):
     got = cn.advect_loop(V0, bases, A, 0.01, steps)
     close(got, orc.advect_loop(V0, A, 0.01, steps))
     assert np.array_equal(got, cn.advect_loop(V0, bases, A, 0.01, steps, use_graph=False))
+
+
+def test_build_nonfinite_with_null_status_does_not_fault(cuda):
+    """cb_tensor_coeffs with a NaN sample and NO status block (the header allows NULL): the
+    non-finite check is skipped instead of writing through a null pointer; the context stays
+    usable (round-1 advice)."""
+    import torch
+
+    from paper_2307_04688_b200 import _lib
+
+    lib = _lib.load()
+    for shape in ((4, 4), (17,) * 4, (13,) * 3):
+        s = np.ones(shape)
+        s.flat[5] = np.nan
+        dev = _lib.to_device(s)
+        coef = _lib.empty((_lib.eval_layout(shape)["elems"],))
+        _lib.check(lib.cb_tensor_coeffs(len(shape), _lib.i64_array(shape), _lib.ptr(dev), _lib.ptr(coef), None,
+                                        _lib.stream_handle()), "tensor_coeffs")
+        torch.cuda.synchronize()
+    close(cn.tensor_coeffs(np.ones((3, 3)), bases_for(2, 3)).coefficients, orc.tensor_coeffs(np.ones((3, 3))))
+
+
+def test_eval_advected_rejects_node_range_outside_grid(cuda):
+    """cb_eval_advected(_peers) validate [node_begin, node_begin + count) against the grid before
+    launching (the peers variant stores into other ranks' buffers)."""
+    import ctypes
+
+    from paper_2307_04688_b200 import _lib
+
+    lib = _lib.load()
+    shape = (5, 5)
+    coef = _lib.empty((_lib.eval_layout(shape)["elems"],))
+    out = _lib.empty((25,))
+    A = _lib.dbl_array(np.zeros(4))
+    lo, hi = _lib.dbl_array([0.0, 0.0]), _lib.dbl_array([1.0, 1.0])
+    for begin, count in ((-1, 3), (20, 6), (0, 26), (3, -1)):
+        rc = lib.cb_eval_advected(2, _lib.i64_array(shape), _lib.ptr(coef), begin, count, A, 0.01, lo, hi, 1,
+                                  _lib.ptr(out), _lib.stream_handle())
+        assert rc == 1 and b"node range" in lib.cb_last_error()
+        dests = (ctypes.c_void_p * 1)(_lib.ptr(out))
+        rc = lib.cb_eval_advected_peers(2, _lib.i64_array(shape), _lib.ptr(coef), begin, count, A, 0.01, lo, hi, 1,
+                                        dests, 1, _lib.stream_handle())
+        assert rc == 1 and b"node range" in lib.cb_last_error()
+    assert lib.cb_eval_advected(2, _lib.i64_array(shape), _lib.ptr(coef), 20, 5, A, 0.01, lo, hi, 1, _lib.ptr(out),
+                                _lib.stream_handle()) == 0
