@@ -155,7 +155,8 @@ def max_over_ranks(x: float, world: int, torch):
         return x
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -500,11 +501,20 @@ def run_ours(args):
     import torch
 
     world, rank, local = dist_setup()
+    # CB_BENCH_SHARE_GPU=1 / CB_BENCH_BACKEND=gloo (tests only): run the multi-rank code path as
+    # several processes on ONE GPU (no kernel waits on another rank: host barriers only); the
+    # numbers of such a run are not a scaling measurement
+    if os.environ.get("CB_BENCH_SHARE_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("CB_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     import paper_2307_04688_b200 as cn
     from paper_2307_04688_b200 import _lib, workloads
     from paper_2307_04688_b200.chebnd import _eval_points_device, tensor_coeffs_device

@@ -1007,7 +1007,13 @@ bool group_build(int ndim, const long long* shape, const double* in, double* out
   // trailing group (pass 1): the largest g (>= q, < ndim) whose slab fits, preferring >= one
   // slab per SM
   int gt = 0;
-  for (int g = std::min(ndim - 1, kGroupMaxG); g >= 1; --g) {
+  // CB_GROUP_MAXG=<1..3> (experiments only): cap the modes per group
+  static const int gmax = [] {
+    const char* e = std::getenv("CB_GROUP_MAXG");
+    const int v = e ? std::atoi(e) : kGroupMaxG;
+    return v < 1 || v > kGroupMaxG ? kGroupMaxG : v;
+  }();
+  for (int g = std::min(ndim - 1, gmax); g >= 1; --g) {
     if (g < q || pw[g] > std::min<long long>(kGroupMaxSlab, max_tile)) continue;
     if (gt == 0) gt = g;
     if (pw[ndim - g] >= sms) { gt = g; break; }
@@ -1039,7 +1045,7 @@ bool group_build(int ndim, const long long* shape, const double* in, double* out
   // leading modes [0, ndim - gt): strided groups, innermost first, in place on the output
   for (int hi = ndim - gt; hi > 0;) {
     int G = 0;
-    while (G < kGroupMaxG && hi - G - 1 >= 0 && pw[G + 1] * 4 <= max_tile) ++G;
+    while (G < gmax && hi - G - 1 >= 0 && pw[G + 1] * 4 <= max_tile) ++G;
     if (G == 0 || np == 3) return false;   // more passes than the plan is worth: per-mode path
     GroupPass& g = plan[np++];
     g = GroupPass{};
