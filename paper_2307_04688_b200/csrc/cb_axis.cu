@@ -316,10 +316,19 @@ __global__ void __launch_bounds__(kF2Threads, 6) fused2_kernel(const __grid_cons
   {
     const long long r0 = static_cast<long long>(blockIdx.x) * kF2RT;
     const int rt_n = static_cast<int>(min(static_cast<long long>(kF2RT), p.R - r0));
+    // cp.async: every element of the tile in flight at once (a load loop serialises on the
+    // global-memory latency: long-scoreboard stalls were 36 % of the last pass's samples)
     for (int e = threadIdx.x; e < N * N * kF2RT; e += blockDim.x) {
       const int row = e / kF2RT, rt = e % kF2RT;
-      sX[e] = (rt < rt_n) ? __ldg(p.in + static_cast<long long>(row) * p.R + r0 + rt) : 0.0;
+      if (rt < rt_n) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(sX + e))),
+                     "l"(p.in + static_cast<long long>(row) * p.R + r0 + rt)
+                     : "memory");
+      } else {
+        sX[e] = 0.0;
+      }
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     // step 1: Z[la][rt][ib] = sum_lb Eb[ib][lb] X[la][lb][rt]; task = (block, chunk), warp-uniform block
 #pragma unroll
