@@ -29,7 +29,8 @@
  *     ordered through that slot by an internal event guard; a cb_eval_grid captured into a CUDA
  *     graph bypasses the guard, so such a graph must not be replayed concurrently with another
  *     cb_eval_grid (captured or eager) on another stream.
- *   - Input range: 1 <= J <= 8 modes, mode sizes 1..4096 (degree <= 4095), at most 2^31
+ *   - Input range: 1 <= J <= 12 modes (the tensor-core evaluators up to J = 8, above that the
+ *     Clenshaw / generic evaluators), mode sizes 1..4096 (degree <= 4095), at most 2^31
  *     elements per tensor.
  */
 #ifndef CHEBNASH_B200_H

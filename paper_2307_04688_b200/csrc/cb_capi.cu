@@ -80,7 +80,7 @@ static int cuda_fail(cudaError_t err, const char* where) {
   } while (0)
 
 static int check_dims(int J, const int64_t* n, const char* fn) {
-  if (J < 1 || J > kMaxDims) return fail(CB_EINVAL, std::string(fn) + ": number of modes must be in [1, 8]");
+  if (J < 1 || J > kMaxDims) return fail(CB_EINVAL, std::string(fn) + ": number of modes must be in [1, 12]");
   if (!n) return fail(CB_EINVAL, std::string(fn) + ": null size array");
   long long total = 1;
   for (int d = 0; d < J; ++d) {

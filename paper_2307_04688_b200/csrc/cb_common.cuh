@@ -14,7 +14,7 @@
 
 namespace cb {
 
-constexpr int kMaxDims = 8;
+constexpr int kMaxDims = 12;
 
 // Status block written by kernels (device) and decoded by the host shim.
 //   w[0] : non-finite input seen (count, saturating)

@@ -535,3 +535,25 @@ def test_eval_advected_rejects_node_range_outside_grid(cuda):
         assert rc == 1 and b"node range" in lib.cb_last_error()
     assert lib.cb_eval_advected(2, _lib.i64_array(shape), _lib.ptr(coef), 20, 5, A, 0.01, lo, hi, 1, _lib.ptr(out),
                                 _lib.stream_handle()) == 0
+
+
+@pytest.mark.parametrize("shape", [(2,) * 9, (3,) * 10, (2, 3) * 6, (4, 3, 2, 2, 3, 2, 2, 3, 2)])
+def test_more_than_eight_modes(cuda, shape):
+    """J = 9..12 modes (the reference has no mode limit): build, scattered evaluation, eval_full,
+    structured evaluation and the advected loop against the oracle."""
+    J = len(shape)
+    rng = np.random.default_rng(J * 31 + sum(shape))
+    s = rng.standard_normal(shape)
+    bases = [cn.make_basis(d - 1, -1.0, 1.0) for d in shape]
+    t = cn.tensor_coeffs(s, bases)
+    C = orc.tensor_coeffs(s)
+    close(t.coefficients, C)
+    pts = 2.0 * rng.random((777, J)) - 1.0
+    close(cn.eval_points(t, pts), orc.eval_points(C, pts))
+    close(cn.eval_full(t, pts[3]), orc.eval_full(C, pts[3]))
+    targets = [np.linspace(-1, 1, 2 + (j % 2)) for j in range(J)]
+    close(cn.eval_grid(t, targets), orc.eval_grid(C, targets))
+    A = rng.uniform(-0.5, 0.5, (J, J))
+    V0 = np.abs(s) + 1.0
+    got = cn.advect_loop(V0, [cn.make_basis(d - 1, 0.0, 1.0) for d in shape], A, 0.01, 2)
+    close(got, orc.advect_loop(V0, A, 0.01, 2))
