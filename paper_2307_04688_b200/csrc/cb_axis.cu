@@ -318,14 +318,26 @@ __global__ void __launch_bounds__(kF2Threads, 6) fused2_kernel(const __grid_cons
     const int rt_n = static_cast<int>(min(static_cast<long long>(kF2RT), p.R - r0));
     // cp.async: every element of the tile in flight at once (a load loop serialises on the
     // global-memory latency: long-scoreboard stalls were 36 % of the last pass's samples)
-    for (int e = threadIdx.x; e < N * N * kF2RT; e += blockDim.x) {
-      const int row = e / kF2RT, rt = e % kF2RT;
-      if (rt < rt_n) {
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(sX + e))),
-                     "l"(p.in + static_cast<long long>(row) * p.R + r0 + rt)
+    // pairs of columns: one 16-byte copy where the global address is 16-byte aligned
+    for (int e2 = threadIdx.x; e2 < N * N * kF2RT / 2; e2 += blockDim.x) {
+      const int row = e2 / (kF2RT / 2), rt = 2 * (e2 % (kF2RT / 2));
+      const double* g = p.in + static_cast<long long>(row) * p.R + r0 + rt;
+      double* d = sX + row * kF2RT + rt;
+      if (rt + 1 < rt_n && (reinterpret_cast<uintptr_t>(g) & 15) == 0) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(d))),
+                     "l"(g)
                      : "memory");
       } else {
-        sX[e] = 0.0;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          if (rt + i < rt_n) {
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(d + i))),
+                         "l"(g + i)
+                         : "memory");
+          } else {
+            d[i] = 0.0;
+          }
+        }
       }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
