@@ -786,7 +786,7 @@ __device__ __forceinline__ void cp_async16(double* dst, const double* src) {
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 template <int TN, int STRIDE, bool CHECK>
-__device__ __forceinline__ void group_fiber(double* s, const double* M, bool& ok) {
+__device__ __forceinline__ void group_fiber(double* s, const double* M, bool& ok, double* dst, long long step) {
   constexpr int N = TN - 1, H = TN / 2, P = H + 1;
   double v[TN];
 #pragma unroll
@@ -812,23 +812,59 @@ __device__ __forceinline__ void group_fiber(double* s, const double* M, bool& ok
 #pragma unroll
       for (int k = 0; k < H; ++k) acc = fma(M[l * P + k], o[k], acc);
     }
-    s[l * STRIDE] = acc;
+    if (dst) dst[l * step] = acc;   // the group's last mode: straight to the output
+    else s[l * STRIDE] = acc;
   }
 }
 
+// The group's last mode writes its outputs straight to global memory (no final barrier and store
+// loop) for the big tiles — three-mode groups or 16-column tiles: 13^6 42.5 -> 37.8 us, 17^5 16.8
+// -> 15.0 us; the small tiles of 17^4 and 33^3 (few CTAs, latency-bound) measured faster through
+// the tile and a row-wise store loop, which they keep.
+template <int TN, int G, int CW>
+constexpr bool group_direct() { return G == 3 || CW == 16; }
+
+// where a tile's output goes (the group's last mode writes to global memory directly)
+struct GroupOut {
+  long long a0;       // contiguous flavour: first slab of the tile
+  long long gbase;    // strided flavour: the tile's first element in the output
+  long long c0;       // strided flavour: the tile's first column
+};
+
 template <int TN, int G, int CW, int g>
-__device__ __forceinline__ void group_mode(double* tile, int nf, const GroupParams<TN>& p, bool& ok) {
+__device__ __forceinline__ void group_mode(double* tile, int nf, const GroupParams<TN>& p, bool& ok,
+                                           const GroupOut& go) {
   constexpr int STRIDE = ipow(TN, G - 1 - g) * CW;
+  constexpr int PG = ipow(TN, G);
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < group_fpt<TN>(); ++j) {
     const int f = threadIdx.x + j * blockDim.x;
     if (f < nf) {
       const int o = f / STRIDE, i = f - (f / STRIDE) * STRIDE;
-      group_fiber<TN, STRIDE, g == G - 1 && CW == 1>(tile + o * TN * STRIDE + i, p.M[g], ok);
+      double* dst = nullptr;
+      long long step = 0;
+      if constexpr (g == 0 && group_direct<TN, G, CW>()) {
+        if constexpr (CW == 1) {
+          const long long a = go.a0 + o;          // slab
+          if (p.K == PG) {                        // one output row per slab
+            dst = p.out + a * p.Kp + i;
+            step = STRIDE;
+          } else {                                // K divides STRIDE
+            dst = p.out + (a * (PG / p.K) + i / p.K) * p.Kp + (i % p.K);
+            step = static_cast<long long>(STRIDE / p.K) * p.Kp;
+          }
+        } else {
+          const int cc = i % CW;
+          if (go.c0 + cc >= p.Cn) continue;       // column past the end
+          dst = p.out + go.gbase + static_cast<long long>(i / CW) * p.Cn + cc;
+          step = static_cast<long long>(ipow(TN, G - 1)) * p.Cn;
+        }
+      }
+      group_fiber<TN, STRIDE, g == G - 1 && CW == 1>(tile + o * TN * STRIDE + i, p.M[g], ok, dst, step);
     }
   }
-  if constexpr (g > 0) group_mode<TN, G, CW, (g > 0 ? g - 1 : 0)>(tile, nf, p, ok);
+  if constexpr (g > 0) group_mode<TN, G, CW, (g > 0 ? g - 1 : 0)>(tile, nf, p, ok, go);
 }
 
 template <int TN, int G, int CW>
@@ -838,6 +874,7 @@ __global__ void __launch_bounds__(group_threads_max<TN>()) group_pass_kernel(con
   const int tid = threadIdx.x, nth = blockDim.x;
   const long long t = blockIdx.x;
   bool ok = true;
+  GroupOut go{};
   if constexpr (CW == 1) {
     // ---------------- contiguous flavour: S whole slabs of the dense input ----------------
     const long long a0 = t * p.S;
@@ -851,31 +888,41 @@ __global__ void __launch_bounds__(group_threads_max<TN>()) group_pass_kernel(con
       for (int e = tid; e < valid; e += nth) cp_async8(tile + e, src + e);
     }
     cp_async_wait_all();
-    // innermost mode first (the per-mode passes' order: bitwise-identical results)
-    group_mode<TN, G, CW, G - 1>(tile, valid / TN, p, ok);
+    go.a0 = a0;
+    // innermost mode first (the per-mode passes' order: bitwise-identical results); the last
+    // mode writes the output rows (pitch Kp) directly
+    group_mode<TN, G, CW, G - 1>(tile, valid / TN, p, ok, go);
     if (p.check_finite && !ok) atomicAdd(&p.st->nonfinite, 1u);   // first mode's loads checked
-    __syncthreads();
-    // rows of K values -> output rows of pitch Kp (pad columns written as zeros)
-    const int rows = valid / p.K;
-    const long long row0 = a0 * P / p.K;
-    double* dst = p.out + row0 * p.Kp;
-    const int n_out = rows * p.Kp;
-    if (p.vec) {
-      for (int z = 2 * tid; z < n_out; z += 2 * nth) {
-        uint32_t row, col;
-        p.fd_Kp.divmod(static_cast<uint32_t>(z), row, col);
-        const double* srow = tile + row * p.K;
-        double2 v;
-        v.x = (static_cast<int>(col) < p.K) ? srow[col] : 0.0;
-        v.y = (static_cast<int>(col) + 1 < p.K) ? srow[col + 1] : 0.0;
-        *reinterpret_cast<double2*>(dst + z) = v;
+    if constexpr (!group_direct<TN, G, CW>()) {
+      // rows of K values -> output rows of pitch Kp (pad columns written as zeros)
+      __syncthreads();
+      const int rows = valid / p.K;
+      double* dst = p.out + (a0 * P / p.K) * p.Kp;
+      const int n_out = rows * p.Kp;
+      if (p.vec) {
+        for (int z = 2 * tid; z < n_out; z += 2 * nth) {
+          uint32_t row, col;
+          p.fd_Kp.divmod(static_cast<uint32_t>(z), row, col);
+          const double* srow = tile + row * p.K;
+          double2 v;
+          v.x = (static_cast<int>(col) < p.K) ? srow[col] : 0.0;
+          v.y = (static_cast<int>(col) + 1 < p.K) ? srow[col + 1] : 0.0;
+          *reinterpret_cast<double2*>(dst + z) = v;
+        }
+      } else {
+        for (int z = tid; z < n_out; z += nth) {
+          uint32_t row, col;
+          p.fd_Kp.divmod(static_cast<uint32_t>(z), row, col);
+          dst[z] = (static_cast<int>(col) < p.K) ? tile[row * p.K + col] : 0.0;
+        }
       }
-    } else {
-      for (int z = tid; z < n_out; z += nth) {
-        uint32_t row, col;
-        p.fd_Kp.divmod(static_cast<uint32_t>(z), row, col);
-        dst[z] = (static_cast<int>(col) < p.K) ? tile[row * p.K + col] : 0.0;
-      }
+    }
+    // pad columns of this tile's output rows
+    const int padw = p.Kp - p.K;
+    if (group_direct<TN, G, CW>() && padw > 0) {
+      const int rows = valid / p.K;
+      double* prow = p.out + (a0 * P / p.K) * p.Kp + p.K;
+      for (int z = tid; z < rows * padw; z += nth) prow[static_cast<long long>(z / padw) * p.Kp + z % padw] = 0.0;
     }
     if (t == 0 && p.R8 > p.R) {
       double* pad = p.out + p.R * p.Kp;
@@ -903,19 +950,24 @@ __global__ void __launch_bounds__(group_threads_max<TN>()) group_pass_kernel(con
       }
     }
     cp_async_wait_all();
-    group_mode<TN, G, CW, G - 1>(tile, E / TN, p, ok);
-    __syncthreads();
-    double* dst = p.out + gbase;
-    if (full && p.vec) {
-      for (int e = 2 * tid; e < E; e += 2 * nth) {
-        const int r = e / CW, cc = e % CW;
-        *reinterpret_cast<double2*>(dst + static_cast<long long>(r) * p.Cn + cc) =
-            *reinterpret_cast<const double2*>(tile + e);
-      }
-    } else {
-      for (int e = tid; e < E; e += nth) {
-        const int r = e / CW, cc = e % CW;
-        if (c0 + cc < p.Cn) dst[static_cast<long long>(r) * p.Cn + cc] = tile[e];
+    go.gbase = gbase;
+    go.c0 = c0;
+    // in place: the tile's inputs are all in shared memory before the last mode stores anything
+    group_mode<TN, G, CW, G - 1>(tile, E / TN, p, ok, go);
+    if constexpr (!group_direct<TN, G, CW>()) {
+      __syncthreads();
+      double* dst = p.out + gbase;
+      if (full && p.vec) {
+        for (int e = 2 * tid; e < E; e += 2 * nth) {
+          const int r = e / CW, cc = e % CW;
+          *reinterpret_cast<double2*>(dst + static_cast<long long>(r) * p.Cn + cc) =
+              *reinterpret_cast<const double2*>(tile + e);
+        }
+      } else {
+        for (int e = tid; e < E; e += nth) {
+          const int r = e / CW, cc = e % CW;
+          if (c0 + cc < p.Cn) dst[static_cast<long long>(r) * p.Cn + cc] = tile[e];
+        }
       }
     }
   }
