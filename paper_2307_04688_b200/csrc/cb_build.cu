@@ -740,8 +740,11 @@ constexpr int kGroupMaxTile = 9216;        // doubles of one tile (72 KB: 2-3 CT
 constexpr int kGroupMaxSlab = 6144;        // contiguous flavour: N^G per slab
 constexpr int kGroupMaxG = 3;
 // fibers per thread per mode: 2 measured faster for n = 13 (13^6: 51 -> 43 us), 1 for 17 and 33
+#ifndef CB_FPT13
+#define CB_FPT13 2
+#endif
 template <int TN>
-constexpr int group_fpt() { return TN == 13 ? 2 : 1; }
+constexpr int group_fpt() { return TN == 13 ? CB_FPT13 : 1; }
 
 // One thread per fiber per mode (nf = E / N threads): straight-line code like the fiber passes
 // (a loop over fibers lets the compiler hoist the ~N^2/2 matrix constants into registers and
@@ -1051,7 +1054,7 @@ bool group_build(int ndim, const long long* shape, const double* in, double* out
   const long long K = evl ? evl->K : 1, Kp = evl ? evl->Kp : 1;
   const long long outsz = evl ? evl->R8 * evl->Kp : total;
   if (outsz >= (1LL << 31) || total >= (1LL << 31)) return false;
-  const int max_threads = (n > 24 ? 256 : 512) * (n == 13 ? 2 : 1);   // fibers per tile and mode
+  const int max_threads = (n > 24 ? 256 : 512) * (n == 13 ? CB_FPT13 : 1);   // fibers per tile and mode
   const long long max_tile = std::min<long long>(kGroupMaxTile, static_cast<long long>(max_threads) * n);
   const int sms = num_sms();
   GroupPass plan[3];
