@@ -164,18 +164,34 @@ struct DmmaSmem {
 // The B operand B[k][p] = prod_{trailing j} T_{l_j(k)}(x_{j,p}) is formed on the fly from the
 // T tables while loading fragments (Q = 1: a plain table read; Q = 2: one DMUL per fragment),
 // so no per-chunk B table has to be built or stored and the smem goes to wide k chunks.
-template <int NCW>
+// Shape codes W (consumer warps, m-tiles x n-tiles per warp):
+//   16 -> 16 warps, 2 x 2, rows 64;   8 -> 8 warps, 2 x 4, two CTAs per SM;
+//   12 -> 8 warps, 4 x 2, rows 64;   28 -> 12 warps, 4 x 2, rows 96;
+//   one accumulator set (epilogue right after its row block) for the rest:
+//   20 -> 8 warps, 4 x 4, rows 128;  24 -> 16 warps, 4 x 2, rows 128;
+//   32 -> 8 warps, 8 x 2, rows 128;  36 -> 12 warps, 8 x 2, rows 192.
+template <int W>
 struct Roles {
-  static constexpr int NT = (NCW == 16) ? 2 : 4;
+  static constexpr int NCW = (W == 16 || W == 24) ? 16 : (W == 28 || W == 36) ? 12 : 8;   // consumer warps
+  static constexpr int NT = (W == 8 || W == 20) ? 4 : 2;
   static constexpr int NGROUPS = 8 / NT;           // n-groups over the 64 points
   static constexpr int MGROUPS = NCW / NGROUPS;    // m-groups over the stage rows
-  static constexpr int MT = 2;
-  static constexpr int ROWS = MGROUPS * MT * 8;    // coefficient rows per stage (64)
+  static constexpr int MT = (W == 16 || W == 8) ? 2 : (W == 32 || W == 36) ? 8 : 4;
+  static constexpr int ROWS = MGROUPS * MT * 8;    // coefficient rows per stage
+  static constexpr bool PINGPONG = (W == 16 || W == 8 || W == 12 || W == 28);
   static constexpr int PRODUCER = NCW;
   static constexpr int BUILDER = NCW + 1;
   static constexpr int THREADS = (NCW + 2) * 32;
-  static constexpr int MIN_BLOCKS = (NCW == 16) ? 1 : 2;
+  static constexpr int MIN_BLOCKS = (W == 8) ? 2 : 1;
 };
+inline int roles_rows(int w) {
+  switch (w) {
+    case 20: case 24: case 32: return 128;
+    case 28: return 96;
+    case 36: return 192;
+    default: return 64;
+  }
+}
 
 __device__ __forceinline__ void consumer_sync_n(int nthreads) {
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
