@@ -121,6 +121,37 @@ def test_eval_points_ragged(cuda, shape, generic):
     close(got, ref, atol=1e-13 * scale)
 
 
+# q = 2 layouts by row count: >= 1,536 rows -> 12 warps x 8 x 2 DMMA tiles (Roles code 36, 192-row
+# stages), >= 192 rows -> 12 warps x 4 x 2 (code 28, 96-row stages), else the 16-warp 2 x 2 shape.
+# The shapes cover NL = 0..6 leading modes and partial last row blocks of every valid-m-tile count.
+@pytest.mark.parametrize("shape,code", [
+    ((6,) * 8, 36), ((5,) * 7, 36), ((7,) * 6, 36), ((40, 41, 6, 7), 36), ((6,) * 7, 36),
+    ((6,) * 6, 28), ((5,) * 6, 28), ((15,) * 4, 28), ((7, 7, 7, 6, 6), 28), ((3, 3, 3, 3, 3, 3, 6, 6), 28),
+    ((13,) * 4, 16), ((20, 6, 6), 16), ((5,) * 5, 16)])
+def test_eval_points_register_tile_shapes(cuda, shape, code):
+    from paper_2307_04688_b200 import _lib
+    from paper_2307_04688_b200.chebnd import _eval_points_device
+
+    rng = np.random.default_rng(sum(shape) * 7 + len(shape))
+    coef = rng.standard_normal(shape)
+    J = len(shape)
+    t = cn.CoefTensor([cn.make_basis(d - 1, -1.0, 1.0) for d in shape], coef)
+    M = 64 * 3 + 37  # ragged last tile
+    pts = rng.uniform(-1.0, 1.0, (M, J))
+    pts[:3] = np.sign(pts[:3])
+    got = _lib.to_host(_eval_points_device(shape, t.device_coefficients, _lib.to_device(pts)))
+    plan = _lib.load().cb_last_eval_plan().decode()
+    assert _lib.eval_layout(shape)["q"] == 2
+    assert f"NCW={code}>" in plan, plan
+    ref = orc.eval_points(coef, pts)
+    scale = max(1.0, float(np.abs(coef).sum()))
+    close(got, ref, atol=1e-13 * scale)
+    # the same points in a different batch split: bitwise identical (shape-only kernel choice)
+    a = _lib.to_host(_eval_points_device(shape, t.device_coefficients, _lib.to_device(pts[:100])))
+    b = _lib.to_host(_eval_points_device(shape, t.device_coefficients, _lib.to_device(pts[100:])))
+    assert np.array_equal(np.concatenate([a, b]), got)
+
+
 def test_eval_points_matches_eval_full(cuda):
     rng = np.random.default_rng(43)
     coef = rng.standard_normal((4, 5, 3))
