@@ -55,7 +55,8 @@ enum {
 int cb_abi_version(void);
 const char* cb_last_error(void);
 
-/* Number of kernels this library has launched in the process (graph replays not included). */
+/* Number of kernels this library has launched in the process, including the kernels of each
+ * cb_advect_loop step-pair graph replay (captured launches count when they are replayed). */
 int64_t cb_kernel_launches(void);
 
 /* Description of the evaluator kernel / plan chosen by the last cb_eval_points or

@@ -514,6 +514,7 @@ struct LoopGraph {
   cudaStream_t cs = nullptr;
   cudaEvent_t ev = nullptr;
   cudaGraphExec_t exec = nullptr;
+  long long kernels = 0;   // kernel launches captured in the step pair (counted per replay)
   unsigned long long last_use = 0;
 };
 constexpr int kLoopGraphCache = 8;
@@ -535,12 +536,16 @@ static cudaError_t loop_graph_build(LoopGraph& g, const EvalLayout& L, const lon
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g.ev, cudaEventDisableTiming);
   cudaGraph_t graph = nullptr;
   if (e == cudaSuccess) e = cudaStreamBeginCapture(g.cs, cudaStreamCaptureModeThreadLocal);
+  const long long launches0 = launch_count();
   if (e == cudaSuccess) {
     cudaError_t e1 = loop_step(L, shape, adv, v, tmp, coef, st, N, g.cs);
     cudaError_t e2 = e1 == cudaSuccess ? loop_step(L, shape, adv, tmp, v, coef, st, N, g.cs) : e1;
     cudaError_t e3 = cudaStreamEndCapture(g.cs, &graph);
     e = e1 != cudaSuccess ? e1 : e2 != cudaSuccess ? e2 : e3;
   }
+  // the captured launches did not run: they count once per replay instead (loop_graph_run)
+  g.kernels = launch_count() - launches0;
+  g_launches.fetch_sub(g.kernels, std::memory_order_relaxed);
   if (e == cudaSuccess) e = cudaGraphInstantiate(&g.exec, graph, 0);
   if (graph) cudaGraphDestroy(graph);
   if (e != cudaSuccess) {
@@ -579,7 +584,10 @@ static cudaError_t loop_graph_run(const EvalLayout& L, const long long* shape, c
   g->last_use = ++g_loop_clock;
   e = cudaEventRecord(g->ev, user);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(g->cs, g->ev, 0);
-  for (int s = 0; s < pairs && e == cudaSuccess; ++s) e = cudaGraphLaunch(g->exec, g->cs);
+  for (int s = 0; s < pairs && e == cudaSuccess; ++s) {
+    e = cudaGraphLaunch(g->exec, g->cs);
+    if (e == cudaSuccess) g_launches.fetch_add(g->kernels, std::memory_order_relaxed);
+  }
   if (e == cudaSuccess) e = cudaEventRecord(g->ev, g->cs);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(user, g->ev, 0);
   return e;

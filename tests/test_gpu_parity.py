@@ -387,6 +387,25 @@ def test_advect_loop(cuda, J, n, steps):
     assert np.array_equal(got, got_ng)
 
 
+def test_advect_loop_counts_graph_replay_kernels(cuda):
+    """cb_kernel_launches counts the kernels of every step-pair graph replay exactly like the
+    eager launches of the same loop (bench.py's gpu_launches for the loop configs)."""
+    from paper_2307_04688_b200 import _lib
+
+    lib = _lib.load()
+    J, n, steps = 3, 9, 8
+    axes = workloads.grid_axes(n, J)
+    V0 = np.exp(sum(np.sin(np.pi * g) for g in np.meshgrid(*axes, indexing="ij")))
+    A = np.full((J, J), 0.1)
+    cn.advect_loop(V0, bases_for(J, n), A, 0.01, steps)  # graph built here (captured launches not counted)
+    c0 = lib.cb_kernel_launches()
+    cn.advect_loop(V0, bases_for(J, n), A, 0.01, steps)
+    c1 = lib.cb_kernel_launches()
+    cn.advect_loop(V0, bases_for(J, n), A, 0.01, steps, use_graph=False)
+    c2 = lib.cb_kernel_launches()
+    assert c1 - c0 == c2 - c1 > 0
+
+
 def test_advect_loop_config3_prefix(cuda):
     w = workloads.make("3", steps=3)
     got = cn.advect_loop(w.values, bases_for(w.J, w.n), w.A, w.dt, w.steps)
