@@ -927,7 +927,14 @@ def run_ours(args):
         e2e_s = max_over_ranks(time.perf_counter() - t0, world, torch)
         e2e = {"value": M * args.steps / e2e_s, "unit": "evals/s", "h2d_bytes_per_step": int(8 * n ** J),
                "d2h_bytes_per_step": int(res.size * 8)}
-        extra = {}
+        # the mode products are FP64-issue co-limited (ncu: FP64 pipe 61-67 % busy in every pass):
+        # n fused multiply-adds per entry of every intermediate and of the output
+        kk = b - a
+        fma = n * sum(kk * k ** (m - 1) * n ** (J - m) for m in range(1, J + 1))
+        tf = 2.0 * fma / (t_total / args.steps) / 1e12
+        extra = {"roofline_fp64": {"bound": "fp64", "pipe": "DFMA (constant-bank matrix operands)", "achieved": tf,
+                                   "peak": peaks["fp64_tflops"], "unit": "TFLOP/s", "frac": tf / peaks["fp64_tflops"],
+                                   "algorithmic": f"2*n*sum_m k^m n^(J-m) = {2 * fma} flops per step"}}
         ms_per_step = 1000.0 * t_total / args.steps
 
     if rank == 0:

@@ -272,6 +272,10 @@ constexpr int kF2RT = 8;       // r' per tile
 constexpr int kF2Warps = 7;    // 7 x 32 = 224 >= 13 * 16 step-1 rows; 3 CTAs / SM
 constexpr int kF2Threads = kF2Warps * 32;
 constexpr int kF2IB = 5;       // K <= 25 (5 blocks)       // outputs per thread item (compile-time constant-bank indices)
+#ifndef CB_F2_IB2
+#define CB_F2_IB2 25
+#endif
+constexpr int kF2IB2 = CB_F2_IB2;   // step 2: outputs per thread item (its N inputs are loaded once per item)
 
 // step 1, output block B: z[ib] for ib in [B*5, B*5+5) from the N inputs v (row la, column rt)
 template <int N, int K, int DA, int B>
@@ -291,8 +295,8 @@ __device__ __forceinline__ void f2_step1(const Fused2Params<N, K, DA>& p, const 
 template <int N, int K, int DA, int B>
 __device__ __forceinline__ void f2_step2(const Fused2Params<N, K, DA>& p, const double* v, double* dst) {
 #pragma unroll
-  for (int j = 0; j < kF2IB; ++j) {
-    const int ia = B * kF2IB + j;
+  for (int j = 0; j < kF2IB2; ++j) {
+    const int ia = B * kF2IB2 + j;
     if (ia < K) {
       double acc = 0.0;
 #pragma unroll
@@ -365,10 +369,11 @@ __global__ void __launch_bounds__(kF2Threads, 6) fused2_kernel(const __grid_cons
     }
     __syncthreads();
     // step 2: out[r0+rt][ia][ib] = sum_la Ea[ia][la] Z[la][rt][ib]; lanes along ib (contiguous)
+    constexpr int NB2 = (K + kF2IB2 - 1) / kF2IB2;
 #pragma unroll
-    for (int it = 0; it < (NB * C2 + kF2Warps - 1) / kF2Warps; ++it) {
+    for (int it = 0; it < (NB2 * C2 + kF2Warps - 1) / kF2Warps; ++it) {
       const int task = warp + it * kF2Warps;
-      if (task >= NB * C2) break;
+      if (task >= NB2 * C2) break;
       const int blk = task / C2, w = (task % C2) * 32 + lane;
       const int rt = w / K, ib = w % K;
       if (w < K * kF2RT && rt < rt_n) {
@@ -378,10 +383,10 @@ __global__ void __launch_bounds__(kF2Threads, 6) fused2_kernel(const __grid_cons
         double* dst = p.out + (r0 + rt) * (K * K) + ib;
         switch (blk) {
           case 0: f2_step2<N, K, DA, 0>(p, v, dst); break;
-          case 1: if constexpr (NB > 1) f2_step2<N, K, DA, 1>(p, v, dst); break;
-          case 2: if constexpr (NB > 2) f2_step2<N, K, DA, 2>(p, v, dst); break;
-          case 3: if constexpr (NB > 3) f2_step2<N, K, DA, 3>(p, v, dst); break;
-          default: if constexpr (NB > 4) f2_step2<N, K, DA, 4>(p, v, dst); break;
+          case 1: if constexpr (NB2 > 1) f2_step2<N, K, DA, 1>(p, v, dst); break;
+          case 2: if constexpr (NB2 > 2) f2_step2<N, K, DA, 2>(p, v, dst); break;
+          case 3: if constexpr (NB2 > 3) f2_step2<N, K, DA, 3>(p, v, dst); break;
+          default: if constexpr (NB2 > 4) f2_step2<N, K, DA, 4>(p, v, dst); break;
         }
       }
     }
