@@ -10,6 +10,8 @@
 //   eval_grid         : J successive rotating mode products with k_j x n_j evaluation matrices
 //                       (the paper's pagemtimes evaluation P:385-417; BASELINE config 5a).
 //   basis_matrix, gather_index, gather_take_f : S/chebnd.py:114-132, 243-272, 97-111.
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -425,6 +427,238 @@ cudaError_t launch_fused2_at(const double* Ea, const double* Eb, bool uploaded, 
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------------------------------
+// Fused pair 13 -> 25 on the FP64 tensor cores (DMMA.8x8x4).  The DFMA form above is issue-bound
+// (2.27 instructions per DFMA, a quarter of them the LDCU.128 uniform loads sm_100 needs for
+// 64-bit constant operands); here a mode product is a 25 x 13 by 13 x (8 columns) GEMM per
+// n-tile: rows 0..23 as 3 DMMA m-tiles over 4 k-steps (l = 13..15 zero-padded), row 24 on DFMA
+// from the SAME B fragments (lane partial over its l = 4 ks + tq, reduced over tq by two
+// shuffles).  The evaluation-matrix fragments live in registers (loaded once per step), so an
+// n-tile of 8 columns issues 12 DMMA + 4 DFMA + 4 LDS + 4 SHFL + stores instead of 81 DFMA +
+// 41 LDCU + loads.  Same tile as the DFMA kernel: in (13, 13, R) -> out (R, 25, 25), 8 r' per tile;
+// step 1 contracts the FIRST mode into shared memory, step 2 the second into global memory, so
+// the DMMA rows of step 2 are ib, contiguous in the output (64-byte runs per store; the other
+// order scattered 8-byte stores over 8 rows: 1.00 vs 0.75 ms).
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ void dmma884_axis(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// A-operand fragments of a 25 x 13 evaluation matrix E (row-major): 3 m-tiles x 4 k-steps for rows
+// 0..23 (zero for l >= 13) and the row-24 entries of this lane's l.
+struct FDFrags {
+  double a[3][4];
+  double e24[4];
+};
+__device__ __forceinline__ void fd_load_frags(const double* __restrict__ E, int gq, int tq, FDFrags& f) {
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const int l = ks * 4 + tq;
+    const bool ok = l < 13;
+#pragma unroll
+    for (int m = 0; m < 3; ++m) f.a[m][ks] = ok ? __ldg(E + (m * 8 + gq) * 13 + l) : 0.0;
+    f.e24[ks] = ok ? __ldg(E + 24 * 13 + l) : 0.0;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Warp-specialised form of the DMMA fused pair: two producer warps run step 1 (first mode) of
+// tile i+1 while four consumer warps run step 2 (second mode) of tile i, each group keeping ITS
+// evaluation-matrix fragments in registers for the whole persistent loop (the one-role form
+// reloaded 16 fragments per thread per step and spent a quarter of its time in tile loads and
+// CTA-wide barriers).  X tiles and the intermediate Z are double-buffered in shared memory; the
+// groups hand Z over with named barriers (bar.arrive / bar.sync, 192 threads).
+// ------------------------------------------------------------------------------------------
+#ifndef CB_WS_P
+#define CB_WS_P 2
+#endif
+#ifndef CB_WS_C
+#define CB_WS_C 4
+#endif
+constexpr int kWSP = CB_WS_P, kWSC = CB_WS_C;           // producer / consumer warps
+constexpr int kWSThreads = (kWSP + kWSC) * 32;
+constexpr int kWSXP = 8, kWSZP = 204;                   // smem pitches (doubles)
+constexpr int kWSCtas = 3;
+
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// Two n-tiles of one GEMM step interleaved (6 independent DMMA chains per warp instead of 3: an
+// n-tile alone is a chain of four dependent k-steps, ~300 cycles of latency for 192 of issue).
+// bptr(i, l) -> shared-memory address of B[l][column gq] of n-tile i; store(i, c, p24) writes it.
+template <typename BPtr, typename Store>
+__device__ __forceinline__ void fd_ntile_pair(const FDFrags& f, int tq, bool two, BPtr bptr, Store store) {
+  double bf[2][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      const int l = ks * 4 + tq;
+      bf[i][ks] = (l < 13 && (i == 0 || two)) ? *bptr(i, l) : 0.0;
+    }
+  double c[2][3][2] = {};
+  double p24[2] = {0.0, 0.0};
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+#pragma unroll
+      for (int m = 0; m < 3; ++m) dmma884_axis(c[i][m][0], c[i][m][1], f.a[m][ks], bf[i][ks]);
+      p24[i] = fma(f.e24[ks], bf[i][ks], p24[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    p24[i] += __shfl_xor_sync(0xffffffffu, p24[i], 1);
+    p24[i] += __shfl_xor_sync(0xffffffffu, p24[i], 2);
+  }
+  store(0, c[0], p24[0]);
+  if (two) store(1, c[1], p24[1]);
+}
+
+__global__ void __launch_bounds__(kWSThreads, kWSCtas)
+    fused2_dmma_ws_kernel(const double* __restrict__ in, double* __restrict__ out, long long R,
+                          const double* __restrict__ Ea, const double* __restrict__ Eb) {
+  constexpr int N = 13, K = 25, RT = kF2RT;
+  constexpr int XS = N * N * kWSXP, ZS = N * kWSZP;
+  extern __shared__ __align__(16) double wssm[];
+  double* sXb = wssm;             // [2][N*N][kWSXP]
+  double* sZb = wssm + 2 * XS;    // [2][N][kWSZP]   (col = rt * 25 + ia)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  const long long ntiles = (R + RT - 1) / RT;
+  if (static_cast<long long>(blockIdx.x) >= ntiles) return;
+  const int n_my = static_cast<int>((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x);  // tiles of this CTA
+  enum { FULL0 = 1, EMPTY0 = 3, PBAR = 5 };
+  FDFrags f;
+  if (warp < kWSP) {
+    // ---------------- producers: X tile loads + step 1 ----------------
+    fd_load_frags(Ea, gq, tq, f);
+    const int ptid = threadIdx.x;   // 0..63
+    auto prefetch = [&](long long tile, double* sX) {
+      const long long r0 = tile * RT;
+      const int rt_n = static_cast<int>(min(static_cast<long long>(RT), R - r0));
+      for (int e2 = ptid; e2 < N * N * RT / 2; e2 += kWSP * 32) {
+        const int row = e2 / (RT / 2), rt = 2 * (e2 % (RT / 2));
+        const double* g = in + static_cast<long long>(row) * R + r0 + rt;
+        double* d = sX + row * kWSXP + rt;
+        if (rt + 1 < rt_n && (reinterpret_cast<uintptr_t>(g) & 15) == 0) {
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(d))),
+                       "l"(g)
+                       : "memory");
+        } else {
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            if (rt + i < rt_n) {
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(d + i))),
+                           "l"(g + i)
+                           : "memory");
+            } else {
+              d[i] = 0.0;
+            }
+          }
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    prefetch(blockIdx.x, sXb);
+    for (int it = 0; it < n_my; ++it) {
+      const int b = it & 1;
+      // both producer warps are done with X buffer b^1 (tile it-1) before it is refilled
+      named_sync(PBAR, kWSP * 32);
+      if (it + 1 < n_my) {
+        prefetch(blockIdx.x + static_cast<long long>(it + 1) * gridDim.x, sXb + (b ^ 1) * XS);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      named_sync(PBAR, kWSP * 32);   // tile `it` visible to both producer warps
+      if (it >= 2) named_sync(EMPTY0 + b, kWSThreads);   // consumers finished Z buffer b (tile it-2)
+      const double* sX = sXb + b * XS;
+      double* sZ = sZb + b * ZS;
+      for (int lb = warp; lb < N; lb += 2 * kWSP) {
+        const int lb2 = lb + kWSP;
+        fd_ntile_pair(
+            f, tq, lb2 < N,
+            [&](int i, int la) { return sX + (la * N + (i ? lb2 : lb)) * kWSXP + gq; },
+            [&](int i, const double (*c)[2], double p24) {
+              double* z = sZ + (i ? lb2 : lb) * kWSZP;
+#pragma unroll
+              for (int m = 0; m < 3; ++m) {
+                z[(2 * tq) * K + m * 8 + gq] = c[m][0];
+                z[(2 * tq + 1) * K + m * 8 + gq] = c[m][1];
+              }
+              if (tq == 0) z[gq * K + 24] = p24;
+            });
+      }
+      named_arrive(FULL0 + b, kWSThreads);
+    }
+  } else {
+    // ---------------- consumers: step 2 + output stores ----------------
+    fd_load_frags(Eb, gq, tq, f);
+    const int cw = warp - kWSP;
+    for (int it = 0; it < n_my; ++it) {
+      const int b = it & 1;
+      const long long r0 = (blockIdx.x + static_cast<long long>(it) * gridDim.x) * RT;
+      const int rt_n = static_cast<int>(min(static_cast<long long>(RT), R - r0));
+      named_sync(FULL0 + b, kWSThreads);
+      const double* sZ = sZb + b * ZS;
+      for (int t = cw; t < (RT * K) / 8; t += 2 * kWSC) {
+        const int t2 = t + kWSC;
+        fd_ntile_pair(
+            f, tq, t2 < (RT * K) / 8,
+            [&](int i, int lb) { return sZ + lb * kWSZP + (i ? t2 : t) * 8 + gq; },
+            [&](int i, const double (*c)[2], double p24) {
+              const int c0 = (i ? t2 : t) * 8;
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                const int col = c0 + 2 * tq + j;
+                const int rt = col / K, ia = col - rt * K;
+                if (rt < rt_n) {
+                  double* dst = out + (r0 + rt) * (K * K) + ia * K + gq;
+#pragma unroll
+                  for (int m = 0; m < 3; ++m) dst[m * 8] = c[m][j];
+                }
+              }
+              if (tq == 0) {
+                const int col = c0 + gq;
+                const int rt = col / K, ia = col - rt * K;
+                if (rt < rt_n) out[(r0 + rt) * (K * K) + ia * K + 24] = p24;
+              }
+            });
+      }
+      // hand Z buffer b back (only if a later tile of this CTA will refill it)
+      if (it + 2 < n_my) named_arrive(EMPTY0 + b, kWSThreads);
+    }
+  }
+}
+
+cudaError_t launch_fused2_dmma_ws(const double* Ea, const double* Eb, const double* in, double* out, long long R,
+                                  cudaStream_t stream) {
+  long long g = (R + kF2RT - 1) / kF2RT;
+  const size_t smem = sizeof(double) * (2 * 13 * 13 * kWSXP + 2 * 13 * kWSZP);
+  ensure_smem_attr(reinterpret_cast<const void*>(fused2_dmma_ws_kernel), 200 * 1024, true);
+  static int per_sm = 0;   // resident CTAs per SM (persistent grid = exactly one wave)
+  if (per_sm == 0) {
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fused2_dmma_ws_kernel, kWSThreads, smem) != cudaSuccess || nb < 1)
+      nb = 1;
+    per_sm = nb;
+    if (std::getenv("CB_GRID_VERBOSE")) std::fprintf(stderr, "fused2_dmma_ws_kernel: %d CTAs/SM, %zu B smem\n", nb, smem);
+  }
+  const long long resident = static_cast<long long>(num_sms()) * per_sm;
+  if (g > resident) g = resident;
+  fused2_dmma_ws_kernel<<<static_cast<unsigned>(g), kWSThreads, smem, stream>>>(in, out, R, Ea, Eb);
+  count_launch();
+  return cudaGetLastError();
+}
+
 template <int N, int K>
 cudaError_t launch_fused2(int d, const double* Ea, const double* Eb, bool uploaded, const double* in, double* out,
                           long long R, cudaStream_t stream) {
@@ -734,7 +968,14 @@ cudaError_t eval_grid(const EvalLayout& L, const double* coef, const long long* 
     if (pair) {
       const long long n = L.n[d], kk = k[d];
       const long long R = total / ((last == J - 1 && L.q == 2) ? L.Kp : n * n);
-      if (n == 13 && kk == 25) err = launch_fused2<13, 25>(d, E[d], E[d + 1], uniform, cur, dst, R, stream);
+      // CB_GRID_MODE=ws selects the DMMA (FP64 tensor core) form of the 13 -> 25 pair: correct
+      // (tested), but slower than the DFMA form so far (0.85 vs 0.63 ms per 25^6 grid), so opt-in
+      static const bool ws = [] {
+        const char* m = std::getenv("CB_GRID_MODE");
+        return m && m[0] == 'w';
+      }();
+      if (n == 13 && kk == 25 && ws) err = launch_fused2_dmma_ws(E[d], E[d + 1], cur, dst, R, stream);
+      else if (n == 13 && kk == 25) err = launch_fused2<13, 25>(d, E[d], E[d + 1], uniform, cur, dst, R, stream);
       else err = launch_fused2<5, 4>(d, E[d], E[d + 1], false, cur, dst, R, stream);
       total = R * kk * kk;
     } else {

@@ -332,6 +332,32 @@ def test_eval_grid(cuda, shape, k):
     close(cn.eval_grid(t, targets), orc.eval_grid(coef, targets))
 
 
+def test_eval_grid_dmma_form_in_subprocess(cuda):
+    """The opt-in FP64 tensor-core form of the fused 13 -> 25 pair (CB_GRID_MODE=ws, read once per
+    process) against the oracle: middle pair, padded last pair (q = 2) and a ragged last tile."""
+    import os
+    import subprocess
+    import sys
+
+    code = r"""
+import numpy as np
+import paper_2307_04688_b200 as cn
+from oracle import cheb_oracle as orc
+for shape, k in (((13, 13, 13, 13), (25, 25, 25, 25)), ((2, 13, 13), (3, 25, 25)), ((7, 3, 13, 13), (5, 4, 25, 25)),
+                 ((13, 13, 3), (25, 25, 5))):
+    rng = np.random.default_rng(sum(shape))
+    coef = rng.standard_normal(shape)
+    t = cn.CoefTensor([cn.make_basis(d - 1, -1.0, 1.0) for d in shape], coef)
+    targets = [np.sort(rng.uniform(-1, 1, kk)) for kk in k]
+    np.testing.assert_allclose(cn.eval_grid(t, targets), orc.eval_grid(coef, targets), rtol=1e-12, atol=1e-11)
+print("ws ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CB_GRID_MODE="ws", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ws ok" in r.stdout, r.stdout + r.stderr
+
+
 @pytest.mark.parametrize("shape,k", [((13, 13, 13, 13), (25, 25, 25, 25)), ((13, 13, 5, 5), (25, 25, 4, 4)),
                                      ((5, 4, 3, 6), (2, 3, 4, 5)), ((13,) * 6, (3, 2, 25, 25, 2, 3))])
 def test_eval_grid_targets_vs_explicit_matrices(cuda, shape, k):
