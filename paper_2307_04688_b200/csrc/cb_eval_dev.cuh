@@ -153,6 +153,8 @@ struct DmmaSmem {
   int src, red, ts, as;   // byte offsets
   int ts_stride;          // doubles per point-table buffer
   int ntab;               // point-table buffers (1 or 2)
+  int tail;               // byte offset of the resident last m-tile (0: none), k-contraction kernel
+  int tail_pitch;         // its row pitch in doubles
 };
 
 // Warp roles (NCW consumer warps + producer + builder):
