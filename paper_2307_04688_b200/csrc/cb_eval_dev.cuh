@@ -206,10 +206,14 @@ __device__ __forceinline__ void consumer_sync_n(int nthreads) {
 #define CB_RC_NT 4
 #endif
 constexpr int kRcNT = CB_RC_NT;                       // n-tiles (8 points) per consumer warp
-constexpr int kRcConsumers = 4 * (8 / kRcNT);         // 4 row groups x (64 / (8 NT)) point groups
+#ifndef CB_RC_RG
+#define CB_RC_RG 4
+#endif
+constexpr int kRcRG = CB_RC_RG;                       // row groups (each kRcRows / kRcRG rows of a stage)
+constexpr int kRcConsumers = kRcRG * (8 / kRcNT);     // row groups x (64 / (8 NT)) point groups
 constexpr int kRcThreads = (kRcConsumers + 3) * 32;
 #ifndef CB_RC_ROWS
-#define CB_RC_ROWS 128
+#define CB_RC_ROWS (32 * CB_RC_RG)
 #endif
 constexpr int kRcRows = CB_RC_ROWS;
 

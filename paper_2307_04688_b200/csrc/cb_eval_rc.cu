@@ -22,7 +22,7 @@ template <int NL, int MTK, int KT>
 __global__ void __launch_bounds__(kRcThreads, 1)
     eval_rc_kernel(const __grid_constant__ EvalParams p, const __grid_constant__ DmmaSmem sm,
                    const __grid_constant__ CUtensorMap amap) {
-  constexpr int NCW = kRcConsumers, NT = kRcNT, kRows = kRcRows, KS = kRows / 16;  // KS k-steps per warp per stage
+  constexpr int NCW = kRcConsumers, NT = kRcNT, kRows = kRcRows, RG = kRcRG, KS = kRows / RG / 4;  // KS k-steps per warp per stage
   constexpr int NGR = 8 / NT;   // point groups (8*NT points each) per row group
   constexpr int J = NL + 1;
   constexpr int KTMAX = (KT < 0) ? 3 : KT;        // DFMA tail columns (compile-time when KT >= 0)
@@ -113,12 +113,19 @@ __global__ void __launch_bounds__(kRcThreads, 1)
       const int ts = it % sm.ntab;
       const int rb = it & 1;
       mbar_wait(&red_full[rb], (it >> 1) & 1);
-      const double* Rb = Red + rb * 8 * kP;
+      const double* Rb = Red + rb * 2 * RG * kP;
       for (int pp = lane; pp < kP; pp += 32) {
         const long long g = tile * kP + pp;
         if (g < p.M) {
-          double v = ((Rb[pp] + Rb[kP + pp]) + Rb[2 * kP + pp]) + Rb[3 * kP + pp];
-          if (KTMAX > 0 && ktail) v += ((Rb[4 * kP + pp] + Rb[5 * kP + pp]) + Rb[6 * kP + pp]) + Rb[7 * kP + pp];
+          double v = Rb[pp];
+#pragma unroll
+          for (int g = 1; g < RG; ++g) v += Rb[g * kP + pp];
+          if (KTMAX > 0 && ktail) {
+            double t = Rb[RG * kP + pp];
+#pragma unroll
+            for (int g = 1; g < RG; ++g) t += Rb[(RG + g) * kP + pp];
+            v += t;
+          }
           emit(p, g, v - Src[ts * kP + pp]);
         }
       }
@@ -155,8 +162,8 @@ __global__ void __launch_bounds__(kRcThreads, 1)
 
     for (int blk = 0; blk < p.nstage_blocks; ++blk) {
       mbar_wait(&bar_full[slot], phase);
-      const double* Ast = As + static_cast<size_t>(slot) * kRows * p.kc + (rg * (kRows / 4) + tq) * p.kc + gq;
-      const int rbase = blk * kRows + rg * (kRows / 4) + tq;   // this lane's row at k-step ks: rbase + 4*ks
+      const double* Ast = As + static_cast<size_t>(slot) * kRows * p.kc + (rg * (kRows / RG) + tq) * p.kc + gq;
+      const int rbase = blk * kRows + rg * (kRows / RG) + tq;   // this lane's row at k-step ks: rbase + 4*ks
       // one k-step: 4 rows of the stage; the row digits come straight from FastDiv (no carries),
       // so the fully-valid case below is straight-line code the scheduler can software-pipeline
       // B fragments W[r][p] of k-step ks for this lane's row r and points pcol + 8*nt (zero past R)
@@ -206,7 +213,7 @@ __global__ void __launch_bounds__(kRcThreads, 1)
           }
         }
       };
-      const int kvalid = min(KS, (static_cast<int>(p.R8) - (blk * kRows + rg * (kRows / 4)) + 3) / 4);  // k-steps with rows < R8
+      const int kvalid = min(KS, (static_cast<int>(p.R8) - (blk * kRows + rg * (kRows / RG)) + 3) / 4);  // k-steps with rows < R8
       if (kvalid == KS) {
         // software-pipelined: the next k-step's W products are formed (and pinned in program
         // order by the volatile asm) before this k-step's DMMAs, hiding the DMUL latency
@@ -270,7 +277,7 @@ __global__ void __launch_bounds__(kRcThreads, 1)
     // hand the tile's partials to the finisher warp (no consumer-wide barrier at the tile end)
     const int rb = it & 1;
     if (it >= 2) mbar_wait(&red_empty[rb], ((it >> 1) & 1) ^ 1);
-    double* Rb = Red + rb * 8 * kP;  // [2][rg: 4 main + 4 tail][P]
+    double* Rb = Red + rb * 2 * RG * kP;  // [2][rg: RG main + RG tail][P]
     if (gq == 0) {
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
@@ -279,7 +286,7 @@ __global__ void __launch_bounds__(kRcThreads, 1)
     }
     if (tq == 0) {
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) Rb[(4 + rg) * kP + pcol + nt * 8] = tv[nt];
+      for (int nt = 0; nt < NT; ++nt) Rb[(RG + rg) * kP + pcol + nt * 8] = tv[nt];
     }
     __syncwarp();
     if (lane == 0) {
