@@ -270,9 +270,19 @@ struct Fused2Params {
   long long R;
 };
 
-constexpr int kF2RT = 8;       // r' per tile
-constexpr int kF2Warps = 7;    // 7 x 32 = 224 >= 13 * 16 step-1 rows; 3 CTAs / SM
+#ifndef CB_F2_RT
+#define CB_F2_RT 8
+#endif
+#ifndef CB_F2_WARPS
+#define CB_F2_WARPS 7
+#endif
+#ifndef CB_F2_MINB
+#define CB_F2_MINB 6
+#endif
+constexpr int kF2RT = CB_F2_RT;         // r' per tile
+constexpr int kF2Warps = CB_F2_WARPS;   // 7 warps x 6 CTAs / SM for 8 r' per tile
 constexpr int kF2Threads = kF2Warps * 32;
+constexpr int kWSRT = 8;                // r' per tile of the DMMA form (its n-tiles are 8 columns)
 constexpr int kF2IB = 5;       // K <= 25 (5 blocks)       // outputs per thread item (compile-time constant-bank indices)
 #ifndef CB_F2_IB2
 #define CB_F2_IB2 25
@@ -309,7 +319,7 @@ __device__ __forceinline__ void f2_step2(const Fused2Params<N, K, DA>& p, const 
 }
 
 template <int N, int K, int DA>
-__global__ void __launch_bounds__(kF2Threads, 6) fused2_kernel(const __grid_constant__ Fused2Params<N, K, DA> p) {
+__global__ void __launch_bounds__(kF2Threads, CB_F2_MINB) fused2_kernel(const __grid_constant__ Fused2Params<N, K, DA> p) {
   extern __shared__ __align__(16) double f2sm[];
   double* sX = f2sm;                   // [N*N][RT]
   double* sZ = f2sm + N * N * kF2RT;   // [N][RT][K]
@@ -525,7 +535,7 @@ __device__ __forceinline__ void fd_ntile_pair(const FDFrags& f, int tq, bool two
 __global__ void __launch_bounds__(kWSThreads, kWSCtas)
     fused2_dmma_ws_kernel(const double* __restrict__ in, double* __restrict__ out, long long R,
                           const double* __restrict__ Ea, const double* __restrict__ Eb) {
-  constexpr int N = 13, K = 25, RT = kF2RT;
+  constexpr int N = 13, K = 25, RT = kWSRT;
   constexpr int XS = N * N * kWSXP, ZS = N * kWSZP;
   extern __shared__ __align__(16) double wssm[];
   double* sXb = wssm;             // [2][N*N][kWSXP]
@@ -641,7 +651,7 @@ __global__ void __launch_bounds__(kWSThreads, kWSCtas)
 
 cudaError_t launch_fused2_dmma_ws(const double* Ea, const double* Eb, const double* in, double* out, long long R,
                                   cudaStream_t stream) {
-  long long g = (R + kF2RT - 1) / kF2RT;
+  long long g = (R + kWSRT - 1) / kWSRT;
   const size_t smem = sizeof(double) * (2 * 13 * 13 * kWSXP + 2 * 13 * kWSZP);
   ensure_smem_attr(reinterpret_cast<const void*>(fused2_dmma_ws_kernel), 200 * 1024, true);
   static int per_sm = 0;   // resident CTAs per SM (persistent grid = exactly one wave)
