@@ -119,11 +119,11 @@ __global__ void __launch_bounds__(kRcThreads, 1)
         if (g < p.M) {
           double v = Rb[pp];
 #pragma unroll
-          for (int g = 1; g < RG; ++g) v += Rb[g * kP + pp];
+          for (int q = 1; q < RG; ++q) v += Rb[q * kP + pp];
           if (KTMAX > 0 && ktail) {
             double t = Rb[RG * kP + pp];
 #pragma unroll
-            for (int g = 1; g < RG; ++g) t += Rb[(RG + g) * kP + pp];
+            for (int q = 1; q < RG; ++q) t += Rb[(RG + q) * kP + pp];
             v += t;
           }
           emit(p, g, v - Src[ts * kP + pp]);
@@ -179,14 +179,14 @@ __global__ void __launch_bounds__(kRcThreads, 1)
             dig[d] = static_cast<int>(l);
             rem = qd;
           }
-          dig[0] = min(static_cast<int>(rem), p.n[0] - 1);  // r >= R: clamp the lookup (weight is zeroed)
+          dig[0] = min(static_cast<int>(rem), p.n[0] - 1);  // r >= R: clamp the lookup (A is zero on those rows)
         }
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
           double v = Tsb[p.toff[0] + dig[0] * kTP + pcol + nt * 8];
 #pragma unroll
           for (int d = 1; d < NL; ++d) v *= Tsb[p.toff[d] + dig[d] * kTP + pcol + nt * 8];
-          w[nt] = (r < R) ? v : 0.0;
+          w[nt] = v;   // rows >= R: A is zero there (layout padding / TMA zero fill), the digits are clamped
         }
       };
       // one k-step: 4 rows of the stage, DMMAs on the DMMA m-tiles + DFMA tail columns
