@@ -142,7 +142,6 @@ __global__ void __launch_bounds__(kRcThreads, 1)
   const int rg = warp / NGR, ng = warp % NGR;
   const int gq = lane >> 2, tq = lane & 3;
   const int pcol = ng * 8 * NT + gq;  // B-fragment column (point) of this lane (+ nt*8)
-  const int R = static_cast<int>(p.R);
   int slot = 0, it = 0;
   unsigned phase = 0;
   for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
