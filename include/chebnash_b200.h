@@ -99,6 +99,15 @@ int cb_transform_axes(int ndim, const int64_t* shape, int a0, int a1, const doub
 int cb_eval_points(int J, const int64_t* n, const double* d_coef, int64_t M, const double* d_points, double* d_out,
                    void* d_status, int flags, void* stream);
 
+/* K1 + K2 in one call — tensor_coeffs chebnd.py:162-190 followed by the evaluation at `M` points
+ * (the per-sweep refit + evaluate of the solver, solver.py:441-449 then :388-397), for loops whose
+ * steps are too small to amortise two launches.  d_values: (n_1..n_J) node values; d_coef receives
+ * the eval-layout coefficients exactly as cb_tensor_coeffs writes them; d_out: (M,) values,
+ * bitwise those of cb_tensor_coeffs + cb_eval_points.  Small J = 2 tensors (modes <= 34, e.g.
+ * BASELINE config 1's 17 x 17) run as ONE fused launch; every other shape as the two calls. */
+int cb_build_eval_points(int J, const int64_t* n, const double* d_values, int64_t M, const double* d_points,
+                         double* d_out, double* d_coef, void* d_status, void* stream);
+
 /* K2 from host buffers — the same evaluation with (M, J) points and (M,) results in HOST memory
  * (pinned for overlap): the points are copied up, evaluated and copied back in chunks on two
  * internal copy streams so the PCIe transfers overlap the evaluator (solver.py:388-397 as called

@@ -66,6 +66,7 @@ SIGNATURES = {
     "cb_tensor_coeffs": (_c_int, [_c_int, _i64p, _vp, _vp, _vp, _vp]),
     "cb_transform_axes": (_c_int, [_c_int, _i64p, _c_int, _c_int, _vp, _vp, _vp, _c_int, _vp]),
     "cb_eval_points": (_c_int, [_c_int, _i64p, _vp, _c_i64, _vp, _vp, _vp, _c_int, _vp]),
+    "cb_build_eval_points": (_c_int, [_c_int, _i64p, _vp, _c_i64, _vp, _vp, _vp, _vp, _vp]),
     "cb_eval_points_host": (_c_int, [_c_int, _i64p, _vp, _c_i64, _vp, _vp, _vp, _vp, _vp, _c_int, _vp]),
     "cb_eval_advected": (_c_int, [_c_int, _i64p, _vp, _c_i64, _c_i64, _dblp, _c_dbl, _dblp, _dblp, _c_int, _vp, _vp]),
     "cb_eval_advected_peers": (

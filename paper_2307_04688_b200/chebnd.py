@@ -392,8 +392,13 @@ class BuildEvalGraph:
         self.kernels_per_replay = int(_lib.load().cb_kernel_launches()) - n0  # own kernels in the graph
 
     def _enqueue(self):
-        tensor_coeffs_device(self.samples, self.shape, out=self.coef)
-        _eval_points_device(self.shape, self.coef, self.points, check=False, out=self.out)
+        # one C-ABI call: a single fused launch for small J = 2 tensors, build + evaluation otherwise
+        _lib.check(
+            _lib.load().cb_build_eval_points(len(self.shape), _lib.i64_array(self.shape), _lib.ptr(self.samples),
+                                             int(self.points.shape[0]), _lib.ptr(self.points), _lib.ptr(self.out),
+                                             _lib.ptr(self.coef), None, _lib.stream_handle()),
+            "build_eval_points",
+        )
 
     def replay(self):
         self.graph.replay()

@@ -209,6 +209,21 @@ int cb_eval_points(int J, const int64_t* n, const double* d_coef, int64_t M, con
   return CB_OK;
 }
 
+int cb_build_eval_points(int J, const int64_t* n, const double* d_values, int64_t M, const double* d_points,
+                         double* d_out, double* d_coef, void* d_status, void* stream) {
+  int rc = check_dims(J, n, "cb_build_eval_points");
+  if (rc) return rc;
+  if (M < 0) return fail(CB_EINVAL, "cb_build_eval_points: negative point count");
+  if (!d_values || !d_coef) return fail(CB_EINVAL, "cb_build_eval_points: null values / coefficient buffer");
+  EvalLayout L = layout_of(J, n);
+  long long shape[kMaxDims];
+  for (int d = 0; d < J; ++d) shape[d] = n[d];
+  CB_CUDA(build_eval_points(L, shape, d_values, M, d_points, d_out, d_coef, static_cast<Status*>(d_status),
+                            static_cast<cudaStream_t>(stream)),
+          "cb_build_eval_points");
+  return CB_OK;
+}
+
 // Copy streams + events for the host-buffer pipeline (one set per device, created on first use).
 namespace {
 constexpr int kPipeMaxChunks = 16;

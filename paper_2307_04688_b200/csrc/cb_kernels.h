@@ -67,6 +67,9 @@ struct AdvectSpec {
   int node_pitch;
 };
 const char* last_eval_plan();  // kernel / plan chosen by the last eval_points on this thread
+// tensor_coeffs + eval_points in one call (one fused launch for small J = 2 tensors)
+cudaError_t build_eval_points(const EvalLayout& L, const long long* shape, const double* values, long long M,
+                              const double* points, double* out, double* coef, Status* st, cudaStream_t stream);
 cudaError_t eval_points(const EvalLayout& L, const double* coef, long long M, const double* points,
                         const AdvectSpec* adv, double* out, Status* st, int force_generic, cudaStream_t stream);
 
