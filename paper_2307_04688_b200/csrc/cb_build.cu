@@ -1083,7 +1083,13 @@ bool group_build(int ndim, const long long* shape, const double* in, double* out
     g.P = static_cast<int>(pw[gt]);
     g.A = pw[ndim - gt];
     int S = 1;
-    while (2LL * S * g.P <= max_tile && (g.A + 2 * S - 1) / (2 * S) >= 2 * sms && S * g.P / n < 256) S *= 2;
+    // CB_GROUP_SMAX=<n> (experiments only): cap the slabs per CTA of the contiguous pass
+    static const int smax = [] {
+      const char* e = std::getenv("CB_GROUP_SMAX");
+      const int v = e ? std::atoi(e) : 0;
+      return v >= 1 ? v : 1 << 20;
+    }();
+    while (2 * S <= smax && 2LL * S * g.P <= max_tile && (g.A + 2 * S - 1) / (2 * S) >= 2 * sms && S * g.P / n < 256) S *= 2;
     if ((g.P & 1) && (S & 1) && S > 1) --S;
     g.S = S;
     g.E = S * g.P;
